@@ -1,0 +1,120 @@
+/* fftcond_b200.h -- C ABI of the B200 FFT field-iteration library.
+ *
+ * Drop-in boundary for the reference solver loops of `fftcond`
+ * (arXiv 2001.08289 companion package).  The reference has no FFI of its
+ * own: its replaceable seam is the private pair
+ *
+ *     _solve_h(pmap, cfg, accelerated)   reference pkg/src/fftcond/solvers.py:280-331
+ *     _solve_aug(pmap, cfg, accelerated) reference pkg/src/fftcond/solvers.py:366-443
+ *
+ * reached through _DISPATCH / solve() (solvers.py:481-491).  fftc_solve()
+ * replaces both loops for d = 2 (the reference's dimension) and d = 3.
+ * Everything above the seam -- SolverConfig validation (solvers.py:110-120),
+ * the reference-medium choice _reference_h / _reference_aug (:221-240,
+ * :334-352), map_t / solve_p (transform.py:99-110, :152-168) -- stays on the
+ * host and only its scalar outputs cross this boundary (fftc_params).
+ *
+ * Plain C types only: no torch, no CUDA types in the signatures (streams are
+ * passed as void*, a cudaStream_t or NULL for the legacy default stream).
+ *
+ * Error convention (mirrors the reference split between exceptions and
+ * numerical outcomes, solvers.py:243-277): parameter errors are raised by the
+ * host layer before the call; a nonzero return code means a CUDA /
+ * allocation / unsupported-shape failure and fftc_last_error() describes it.
+ * Converged / MaxIters / Diverged / degenerate-flux are RESULTS, returned in
+ * fftc_result, never errors.
+ */
+#ifndef FFTCOND_B200_H
+#define FFTCOND_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* schemes: same order as reference transform.py:23-39 (SchemeKind) */
+enum { FFTC_BASIC = 0, FFTC_EM = 1, FFTC_BASIC_SUB = 2, FFTC_EM_SUB = 3 };
+/* termination: reference solvers.py:54-57 (TerminationStatus) */
+enum { FFTC_CONVERGED = 0, FFTC_MAX_ITERS = 1, FFTC_DIVERGED = 2 };
+
+typedef struct fftc_problem {
+  int32_t d;          /* 2 or 3 */
+  int32_t reserved;
+  int64_t n[3];       /* n[0] = nx (fastest), n[1] = ny, n[2] = nz (1 for d = 2) */
+  const uint8_t* chi; /* DEVICE pointer, nz*ny*nx bytes, 1 = phase 1 (PhaseMap.chi, geometry.py:20-39) */
+} fftc_problem;
+
+typedef struct fftc_params {
+  int32_t scheme;       /* FFTC_* */
+  int32_t reserved;
+  double sigma1[2];     /* inclusion conductivity (re, im)            SolverConfig.sigma1 */
+  double sigma0[2];     /* reference medium from _reference_h/_aug    solvers.py:221,334 */
+  double t[2];          /* map_t(sigma1) (substituted schemes)        transform.py:99 */
+  double p1[2], p2[2], p3[2]; /* solve_p(interval)                    transform.py:152 */
+  double e0[3][2];      /* applied field, d complex components        SolverConfig.e0 */
+  double tol;           /* SolverConfig.tol */
+  int64_t max_iters;    /* SolverConfig.max_iters */
+  double gamma1_scale;  /* test hook, reference spectral_ops.py:29-30 (1.0) */
+} fftc_params;
+
+typedef struct fftc_result {
+  int32_t status;          /* FFTC_CONVERGED / FFTC_MAX_ITERS / FFTC_DIVERGED */
+  int32_t degenerate_flux; /* SolveResult.degenerate_flux */
+  int64_t iterations;      /* len(history) */
+  double sigma_star[2];    /* last recorded sigma* (or last evaluated if none, solvers.py:323) */
+  double mean_E[3][2];     /* compensated-style mean of the returned E field */
+  double mean_J[3][2];     /* mean of the returned J field */
+  int64_t kernel_launches; /* number of library kernels launched by this call */
+  double device_ms;        /* device time of the solve (CUDA events) */
+} fftc_result;
+
+/* Run one solve on the device.
+ *   history : HOST buffer of history_cap records x 3 doubles
+ *             (sigma*_re, sigma*_im, residual); record k-1 is iteration k.
+ *   E, J    : nullable DEVICE buffers of d*N complex128 (component-major,
+ *             layout (c, z, y, x) like VectorField.data, spectral_ops.py:58-70)
+ *   aug     : nullable DEVICE buffer of 3*d*N complex128, (Q, S, T) of the
+ *             substituted schemes (SolveResult.aug_field)
+ *   stream  : cudaStream_t or NULL.
+ * Returns 0 on success. */
+int fftc_solve(const fftc_problem* problem, const fftc_params* params, double* history,
+               int64_t history_cap, void* E, void* J, void* aug, fftc_result* out, void* stream);
+
+/* Same contract, host-resident chi and outputs (the library copies in and
+ * out; E/J/aug host buffers are nullable).  For FFI users without a device
+ * allocator. */
+int fftc_solve_host(const fftc_problem* problem_with_host_chi, const fftc_params* params,
+                    double* history, int64_t history_cap, void* E_host, void* J_host,
+                    void* aug_host, fftc_result* out);
+
+/* Operator API on DEVICE fields of d*N complex128 (layout as above).
+ *
+ * fftc_fft: in-place unnormalised DFT of every component along each axis in
+ * axes_mask (bit 0 = x, 1 = y, 2 = z); inverse != 0 uses exp(+i...).
+ * Building block of numpy.fft.fftn/ifftn as called by the reference
+ * (spectral_ops.py:123,128).
+ *
+ * fftc_gamma1: out = Gamma_1(in), the curl-free zero-mean projection with
+ * multiplier k k^T/|k|^2 * scale (k = 0 dropped, Nyquist kept), replacing
+ * _gamma1_arr (spectral_ops.py:120-128); scale mirrors the _gamma1_scale
+ * test hook (:29-30).  in may equal out. */
+int fftc_fft(const fftc_problem* problem, void* data, int32_t inverse, int32_t axes_mask, void* stream);
+int fftc_gamma1(const fftc_problem* problem, const void* in, void* out, double scale, void* stream);
+
+/* 1 if an axis of length n is supported by the compiled transforms. */
+int fftc_supported_length(int64_t n);
+
+/* Description of the last error on this thread ("" if none). */
+const char* fftc_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int fftc_version(void);
+
+/* Total kernels launched by this library in this process. */
+int64_t fftc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTCOND_B200_H */

@@ -1,0 +1,708 @@
+// abi.cu -- C-ABI entry points and the host driver of the iteration.
+//
+// fftc_solve() replaces the reference loops _solve_h / _solve_aug
+// (reference solvers.py:280-331, :366-443).  Per iteration it launches the
+// fused sweeps of sweeps.cuh; the stopping monitor runs on the device, so
+// the host only synchronises once per chunk of iterations to collect the
+// history ring and the stop flag.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fftcond_b200.h"
+#include "kernel_table.h"
+#include "sweeps.cuh"
+
+using namespace fftc;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+struct Registry {
+  std::mutex mu;
+  bool filled = false;
+  LTable tab[MAX_LG + 1];
+  const double2* tw[MAX_LG + 1] = {};  // device twiddle tables per length
+  int num_sms = 0;
+  int device = -1;
+};
+Registry& reg() {
+  static Registry r;
+  return r;
+}
+
+#define CK(expr)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      g_err = std::string(#expr) + ": " + cudaGetErrorString(e_);                     \
+      return 1;                                                                       \
+    }                                                                                 \
+  } while (0)
+
+int lg2_exact(long long n) {
+  if (n < 2 || (n & (n - 1))) return -1;
+  int lg = 0;
+  while ((1LL << lg) < n) ++lg;
+  return lg <= MAX_LG ? lg : -1;
+}
+
+// exp(-2 pi i m / L), m = 0..L-1, in long double then rounded
+std::vector<double2> make_twiddles(int L) {
+  std::vector<double2> h(L);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int m = 0; m < L; ++m) {
+    // reduce by symmetry to keep the argument small
+    long double ang = 2.0L * pi * (long double)m / (long double)L;
+    h[m].x = (double)cosl(ang);
+    h[m].y = (double)(-sinl(ang));
+  }
+  // exact values at the quadrant points
+  h[0] = make_double2(1.0, 0.0);
+  if (L % 4 == 0) {
+    h[L / 4] = make_double2(0.0, -1.0);
+    h[3 * L / 4] = make_double2(0.0, 1.0);
+  }
+  if (L % 2 == 0) h[L / 2] = make_double2(-1.0, 0.0);
+  return h;
+}
+
+int ensure_registry() {
+  Registry& r = reg();
+  std::lock_guard<std::mutex> lk(r.mu);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (r.filled && r.device == dev) return 0;
+  fftc_fill_table_1(r.tab[1]);
+  fftc_fill_table_2(r.tab[2]);
+  fftc_fill_table_3(r.tab[3]);
+  fftc_fill_table_4(r.tab[4]);
+  fftc_fill_table_5(r.tab[5]);
+  fftc_fill_table_6(r.tab[6]);
+  fftc_fill_table_7(r.tab[7]);
+  fftc_fill_table_8(r.tab[8]);
+  fftc_fill_table_9(r.tab[9]);
+  fftc_fill_table_10(r.tab[10]);
+  fftc_fill_table_11(r.tab[11]);
+  fftc_fill_table_12(r.tab[12]);
+  CK(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  for (int lg = 1; lg <= MAX_LG; ++lg) {
+    LTable& t = r.tab[lg];
+    KInfo* all[4 + 4 + KC_COUNT + 2];
+    int n = 0;
+    all[n++] = &t.row_fwd;
+    all[n++] = &t.row_inv;
+    for (int s = 0; s < 4; ++s) all[n++] = &t.s1[s];
+    for (int s = 0; s < 4; ++s) all[n++] = &t.s3[s];
+    for (int c = 0; c < KC_COUNT; ++c) all[n++] = &t.col[c];
+    for (int i = 0; i < n; ++i) {
+      KInfo* k = all[i];
+      if (k->smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
+        if (e != cudaSuccess) {  // too large for this device: mark unusable
+          cudaGetLastError();
+          k->max_active = 0;
+          continue;
+        }
+      }
+      int nb = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k->fn, k->threads, k->smem));
+      k->max_active = nb;
+    }
+    if (!r.tw[lg]) {
+      std::vector<double2> h = make_twiddles(1 << lg);
+      double2* d = nullptr;
+      CK(cudaMalloc(&d, sizeof(double2) * h.size()));
+      CK(cudaMemcpy(d, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
+      r.tw[lg] = d;
+    }
+  }
+  r.device = dev;
+  r.filled = true;
+  return 0;
+}
+
+double2 C2(const double* p) { return make_double2(p[0], p[1]); }
+double2 hmul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+double2 hadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+double2 hsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+double2 hinv(double2 a) {  // 1 / a (Smith)
+  if (fabs(a.x) >= fabs(a.y)) {
+    double r = a.y / a.x, den = a.x + a.y * r;
+    return make_double2(1.0 / den, -r / den);
+  }
+  double r = a.x / a.y, den = a.x * r + a.y;
+  return make_double2(r / den, -1.0 / den);
+}
+double2 hdiv(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    double r = b.y / b.x, den = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+  }
+  double r = b.x / b.y, den = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+
+struct Launcher {
+  cudaStream_t s;
+  int num_sms;
+  long long count = 0;
+  int go(const KInfo& k, long long work_lines, void** args) {
+    if (!k.fn || k.max_active <= 0) {
+      g_err = "kernel configuration unavailable on this device (shared memory)";
+      return 1;
+    }
+    long long need = (work_lines + k.lines - 1) / k.lines;
+    long long cap = (long long)k.max_active * num_sms;
+    unsigned grid = (unsigned)(need < cap ? need : cap);
+    if (grid < 1) grid = 1;
+    CK(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.threads), args, (size_t)k.smem, s));
+    ++count;
+    return 0;
+  }
+};
+
+template <class F>
+int launch_elementwise(F* fn, Launcher& L, long long total, Args& a) {
+  void* args[] = {&a};
+  int per = 256;
+  long long need = (total + per - 1) / per;
+  long long cap = (long long)L.num_sms * 8;
+  unsigned grid = (unsigned)(need < cap ? need : cap);
+  if (grid < 1) grid = 1;
+  CK(cudaLaunchKernel((const void*)fn, dim3(grid), dim3(per), args, 0, L.s));
+  ++L.count;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fftc_last_error(void) { return g_err.c_str(); }
+int fftc_version(void) { return 100; }
+int64_t fftc_launch_count(void) { return g_launches.load(); }
+int fftc_supported_length(int64_t n) { return lg2_exact(n) > 0 ? 1 : 0; }
+
+int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, int64_t history_cap,
+               void* E, void* J, void* aug, fftc_result* out, void* stream) {
+  g_err.clear();
+  if (!pb || !pr || !out) {
+    g_err = "null argument";
+    return 2;
+  }
+  const int d = pb->d;
+  if (d != 2 && d != 3) {
+    g_err = "d must be 2 or 3";
+    return 2;
+  }
+  const long long nx = pb->n[0], ny = pb->n[1], nz = d == 3 ? pb->n[2] : 1;
+  const int lgx = lg2_exact(nx), lgy = lg2_exact(ny), lgz = d == 3 ? lg2_exact(nz) : 0;
+  if (lgx < 0 || lgy < 0 || lgz < 0) {
+    g_err = "unsupported grid: every axis must be a power of two in [2, 4096]";
+    return 3;
+  }
+  if (pr->scheme < 0 || pr->scheme > 3) {
+    g_err = "bad scheme";
+    return 2;
+  }
+  if (ensure_registry()) return 1;
+  Registry& R = reg();
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long N = nx * ny * nz;
+  const int scheme = pr->scheme;
+  const bool aug_s = scheme >= 2;
+
+  // ---- scalars (host side, mirroring the reference expressions) ----
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.d = d;
+  a.nx = (int)nx;
+  a.ny = (int)ny;
+  a.nz = (int)nz;
+  a.N = N;
+  a.chi = pb->chi;
+  a.sigma1 = C2(pr->sigma1);
+  a.s0 = C2(pr->sigma0);
+  double e0sq = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    a.e0[c] = c < d ? C2(pr->e0[c]) : make_double2(0, 0);
+    e0sq += a.e0[c].x * a.e0[c].x + a.e0[c].y * a.e0[c].y;
+  }
+  a.e0sq = e0sq;
+  a.tol = pr->tol;
+  a.inv_n = 1.0 / (double)N;
+  a.gscale = pr->gamma1_scale;
+  a.max_iters = pr->max_iters;
+  const double2 one = make_double2(1.0, 0.0);
+  a.inv_s0 = hinv(a.s0);
+  a.sum1 = hadd(a.sigma1, a.s0);
+  a.sum2 = hadd(one, a.s0);
+  a.inv_sum1 = hinv(a.sum1);
+  a.inv_sum2 = hinv(a.sum2);
+  a.sm1 = hsub(a.sigma1, a.s0);
+  a.sm2 = hsub(one, a.s0);
+  const double2 two_s0 = make_double2(2.0 * a.s0.x, 2.0 * a.s0.y);
+  for (int c = 0; c < 3; ++c) a.two_s0_e0[c] = hmul(two_s0, a.e0[c]);
+  const double2 t = C2(pr->t);
+  a.p1 = C2(pr->p1);
+  a.p2 = C2(pr->p2);
+  a.p3 = C2(pr->p3);
+  const double2 tm1 = hsub(t, one);
+  a.tm1p1 = hmul(tm1, a.p1);
+  a.tm1p2 = hmul(tm1, a.p2);
+  a.tm1p3 = hmul(tm1, a.p3);
+  a.cq = hmul(a.p1, a.tm1p1);
+  a.cs = hmul(a.p2, a.tm1p1);
+  a.sinv = hdiv(one, hadd(one, a.s0));         // inv_scale = 1/(1+s0)   (solvers.py:388)
+  const double2 cinv = hdiv(tm1, hadd(t, a.s0));  // inv_c = (t-1)/(t+s0)  (solvers.py:389)
+  a.cinv_p1 = hmul(cinv, a.p1);
+  a.cinv_p2 = hmul(cinv, a.p2);
+  a.cinv_p3 = hmul(cinv, a.p3);
+
+  // ---- workspace ----
+  const int nslots = scheme == FFTC_EM_SUB ? 3 : (scheme == FFTC_BASIC_SUB ? 2 : 1);
+  const size_t fld = sizeof(double2) * (size_t)d * N;
+  const int hist_ring = 1024;
+  const size_t partial_cap = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
+  char* ws = nullptr;
+  const size_t ws_bytes = fld * (nslots + 2) + sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring +
+                          sizeof(DevState) + 4096;
+  CK(cudaMallocAsync((void**)&ws, ws_bytes, s));
+  size_t o = 0;
+  auto carve = [&](size_t bytes) {
+    char* p = ws + o;
+    o += (bytes + 255) & ~(size_t)255;
+    return p;
+  };
+  for (int i = 0; i < nslots; ++i) a.X[i] = (double2*)carve(fld);
+  a.A = (double2*)carve(fld);
+  a.B = (double2*)carve(fld);
+  a.partials = (double*)carve(sizeof(double) * partial_cap);
+  a.history = (double*)carve(sizeof(double) * 3 * hist_ring);
+  a.hist_cap = hist_ring;
+  a.st = (DevState*)carve(sizeof(DevState));
+  a.outE = (double2*)E;
+  a.outJ = (double2*)J;
+  a.outAug = (double2*)aug;
+  a.tw[0] = R.tw[lgx];
+  a.tw[1] = R.tw[lgy];
+  a.tw[2] = d == 3 ? R.tw[lgz] : R.tw[lgy];
+
+  int rc = 0;
+  cudaEvent_t ev0, ev1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  DevState* hst = nullptr;
+  CK(cudaMallocHost((void**)&hst, sizeof(DevState)));
+  Launcher Lc{s, R.num_sms};
+  const LTable& TX = R.tab[lgx];
+  const LTable& TY = R.tab[lgy];
+  const LTable& TZ = R.tab[d == 3 ? lgz : lgy];
+  long long nrec_host = 0;
+  bool stopped = false;
+
+  do {
+    CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
+    CK(cudaEventRecord(ev0, s));
+    switch (scheme) {
+      case FFTC_BASIC: rc = launch_elementwise(k_init<BASIC>, Lc, (long long)d * N, a); break;
+      case FFTC_EM: rc = launch_elementwise(k_init<EM>, Lc, (long long)d * N, a); break;
+      case FFTC_BASIC_SUB: rc = launch_elementwise(k_init<BASIC_SUB>, Lc, (long long)d * N, a); break;
+      default: rc = launch_elementwise(k_init<EM_SUB>, Lc, (long long)d * N, a); break;
+    }
+    if (rc) break;
+
+    // column geometries
+    ColGeom mid{};
+    ColGeom yf{};
+    const bool em_type = (scheme == FFTC_EM || scheme == FFTC_EM_SUB);
+    const KInfo* kmid;
+    if (d == 2) {
+      mid.axis = 1;
+      mid.nouter = 1;
+      mid.stride = nx;
+      mid.ostride = 0;
+      mid.nstrips = (int)(nx / TY.col_w);
+      kmid = &TY.col[em_type ? KC_MID2_EM : KC_MID2_BASIC];
+    } else {
+      mid.axis = 2;
+      mid.nouter = (int)ny;
+      mid.stride = nx * ny;
+      mid.ostride = nx;
+      mid.nstrips = (int)(nx / TZ.col3_w);
+      kmid = &TZ.col[em_type ? KC_MID3_EM : KC_MID3_BASIC];
+      yf.axis = 1;
+      yf.nouter = (int)nz;
+      yf.stride = nx;
+      yf.ostride = nx * ny;
+      yf.nstrips = (int)(nx / 2);
+    }
+    const long long mid_lines = (long long)mid.nouter * mid.nstrips * (em_type ? 2 : 1);
+    const long long row_lines = (long long)d * ny * nz;
+    const long long yf_lines = (long long)yf.nouter * yf.nstrips * d;
+    void* a1[] = {&a};
+    void* amid[] = {&a, &mid};
+    ColGeom yfB = yf;  // forward y pass of field B (em-type) uses the same geometry
+
+    long long chunk = 2;
+    long long launched_iters = 0;
+    while (!stopped) {
+      long long todo = chunk;
+      if (launched_iters + todo > pr->max_iters) todo = pr->max_iters - launched_iters;
+      for (long long it = 0; it < todo && !rc; ++it) {
+        rc = Lc.go(TX.s1[scheme], row_lines, a1);
+        if (rc) break;
+        if (d == 3) {
+          // y forward of field A (and B for em-type) -- plain column pass
+          Args aB = a;
+          void* ayf[] = {&a, &yf};
+          rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf);
+          if (rc) break;
+          if (em_type) {
+            aB.A = a.B;
+            void* ab[] = {&aB, &yfB};
+            rc = Lc.go(TY.col[KC_FWD], yf_lines, ab);
+            if (rc) break;
+          }
+        }
+        rc = Lc.go(*kmid, mid_lines, amid);
+        if (rc) break;
+        if (d == 3) {
+          void* ai[] = {&a, &yf};
+          rc = Lc.go(TY.col[KC_INV], yf_lines, ai);
+          if (rc) break;
+        }
+        rc = Lc.go(TX.s3[scheme], row_lines, a1);
+      }
+      if (rc) break;
+      launched_iters += todo;
+      CK(cudaMemcpyAsync(hst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      // collect new history records from the device ring
+      long long nrec = hst->nrec;
+      if (nrec > history_cap) {
+        g_err = "history buffer too small";
+        rc = 4;
+        break;
+      }
+      for (long long r0 = nrec_host; r0 < nrec;) {
+        long long slot = r0 % hist_ring;
+        long long cnt = std::min(nrec - r0, (long long)hist_ring - slot);
+        CK(cudaMemcpy(history + 3 * r0, a.history + 3 * slot, sizeof(double) * 3 * cnt, cudaMemcpyDeviceToHost));
+        r0 += cnt;
+      }
+      nrec_host = nrec;
+      stopped = hst->stopped != 0 || launched_iters >= pr->max_iters;
+      chunk = std::min<long long>(chunk * 2, 256);
+    }
+    if (rc) break;
+    switch (scheme) {
+      case FFTC_BASIC: rc = launch_elementwise(k_finalize<BASIC>, Lc, (long long)d * N, a); break;
+      case FFTC_EM: rc = launch_elementwise(k_finalize<EM>, Lc, (long long)d * N, a); break;
+      case FFTC_BASIC_SUB: rc = launch_elementwise(k_finalize<BASIC_SUB>, Lc, (long long)d * N, a); break;
+      default: rc = launch_elementwise(k_finalize<EM_SUB>, Lc, (long long)d * N, a); break;
+    }
+    if (rc) break;
+    CK(cudaEventRecord(ev1, s));
+    CK(cudaMemcpyAsync(hst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    out->device_ms = ms;
+    out->status = hst->status;
+    out->degenerate_flux = hst->degenerate;
+    out->iterations = hst->nrec;
+    if (hst->nrec > 0) {
+      out->sigma_star[0] = history[3 * (hst->nrec - 1) + 0];
+      out->sigma_star[1] = history[3 * (hst->nrec - 1) + 1];
+    } else {
+      out->sigma_star[0] = hst->last_sstar.x;
+      out->sigma_star[1] = hst->last_sstar.y;
+    }
+    for (int c = 0; c < 3; ++c) {
+      out->mean_E[c][0] = c < d ? hst->meanE[c].x : 0.0;
+      out->mean_E[c][1] = c < d ? hst->meanE[c].y : 0.0;
+      out->mean_J[c][0] = c < d ? hst->meanJ[c].x : 0.0;
+      out->mean_J[c][1] = c < d ? hst->meanJ[c].y : 0.0;
+    }
+  } while (0);
+  out->kernel_launches = Lc.count;
+  g_launches += Lc.count;
+  cudaFreeAsync(ws, s);
+  cudaFreeHost(hst);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (!rc) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      g_err = cudaGetErrorString(e);
+      rc = 1;
+    }
+  }
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// operator API: plain transforms and the Gamma_1 projection on device fields
+// ---------------------------------------------------------------------------
+namespace {
+struct GridInfo {
+  int d, lgx, lgy, lgz;
+  long long nx, ny, nz, N;
+};
+int grid_info(const fftc_problem* pb, GridInfo& g) {
+  if (!pb || (pb->d != 2 && pb->d != 3)) {
+    g_err = "d must be 2 or 3";
+    return 2;
+  }
+  g.d = pb->d;
+  g.nx = pb->n[0];
+  g.ny = pb->n[1];
+  g.nz = g.d == 3 ? pb->n[2] : 1;
+  g.lgx = lg2_exact(g.nx);
+  g.lgy = lg2_exact(g.ny);
+  g.lgz = g.d == 3 ? lg2_exact(g.nz) : 0;
+  if (g.lgx < 0 || g.lgy < 0 || g.lgz < 0) {
+    g_err = "unsupported grid: every axis must be a power of two in [2, 4096]";
+    return 3;
+  }
+  g.N = g.nx * g.ny * g.nz;
+  return 0;
+}
+
+// scratch state for kernels that end in a reduction
+struct Scratch {
+  char* ws = nullptr;
+  cudaStream_t s = nullptr;
+  int alloc(Args& a, int num_sms, cudaStream_t st) {
+    s = st;
+    const size_t pc = (size_t)num_sms * 64 * NQMAX + 16 * NQMAX;
+    const size_t bytes = sizeof(double) * pc + sizeof(double) * 3 * 16 + sizeof(DevState) + 1024;
+    CK(cudaMallocAsync((void**)&ws, bytes, s));
+    CK(cudaMemsetAsync(ws, 0, bytes, s));
+    a.partials = (double*)ws;
+    a.history = (double*)(ws + ((sizeof(double) * pc + 255) & ~(size_t)255));
+    a.hist_cap = 16;
+    a.st = (DevState*)((char*)a.history + 512);
+    return 0;
+  }
+  ~Scratch() {
+    if (ws) cudaFreeAsync(ws, s);
+  }
+};
+
+int run_axis(Launcher& Lc, Args& a, const GridInfo& g, int axis, bool inverse, double scale) {
+  Registry& R = reg();
+  if (axis == 0) {
+    const KInfo& k = inverse ? R.tab[g.lgx].row_inv : R.tab[g.lgx].row_fwd;
+    void* args[] = {&a, &scale};
+    return Lc.go(k, (long long)g.d * g.ny * g.nz, args);
+  }
+  ColGeom gm{};
+  int lg;
+  if (axis == 1) {
+    lg = g.lgy;
+    gm.axis = 1;
+    gm.nouter = (int)g.nz;
+    gm.stride = g.nx;
+    gm.ostride = g.nx * g.ny;
+  } else {
+    lg = g.lgz;
+    gm.axis = 2;
+    gm.nouter = (int)g.ny;
+    gm.stride = g.nx * g.ny;
+    gm.ostride = g.nx;
+  }
+  gm.nstrips = (int)(g.nx / 2);
+  void* args[] = {&a, &gm};
+  const KInfo& k = R.tab[lg].col[inverse ? KC_INV : KC_FWD];
+  return Lc.go(k, (long long)gm.nouter * gm.nstrips * g.d, args);
+}
+}  // namespace
+
+int fftc_fft(const fftc_problem* pb, void* data, int32_t inverse, int32_t axes_mask, void* stream) {
+  g_err.clear();
+  GridInfo g;
+  if (int rc = grid_info(pb, g)) return rc;
+  if (ensure_registry()) return 1;
+  Registry& R = reg();
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.d = g.d;
+  a.nx = (int)g.nx;
+  a.ny = (int)g.ny;
+  a.nz = (int)g.nz;
+  a.N = g.N;
+  a.A = (double2*)data;
+  a.op_mode = 1;
+  a.tw[0] = R.tw[g.lgx];
+  a.tw[1] = R.tw[g.lgy];
+  a.tw[2] = g.d == 3 ? R.tw[g.lgz] : R.tw[g.lgy];
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc;
+  if (sc.alloc(a, R.num_sms, s)) return 1;
+  Launcher Lc{s, R.num_sms};
+  for (int ax = 0; ax < g.d; ++ax)
+    if (axes_mask & (1 << ax))
+      if (int rc = run_axis(Lc, a, g, ax, inverse != 0, 1.0)) return rc;
+  g_launches += Lc.count;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int fftc_gamma1(const fftc_problem* pb, const void* in, void* out, double scale, void* stream) {
+  g_err.clear();
+  GridInfo g;
+  if (int rc = grid_info(pb, g)) return rc;
+  if (ensure_registry()) return 1;
+  Registry& R = reg();
+  cudaStream_t s = (cudaStream_t)stream;
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.d = g.d;
+  a.nx = (int)g.nx;
+  a.ny = (int)g.ny;
+  a.nz = (int)g.nz;
+  a.N = g.N;
+  a.inv_n = 1.0 / (double)g.N;
+  a.gscale = scale;
+  a.A = (double2*)out;
+  a.B = (double2*)out;
+  a.tw[0] = R.tw[g.lgx];
+  a.tw[1] = R.tw[g.lgy];
+  a.tw[2] = g.d == 3 ? R.tw[g.lgz] : R.tw[g.lgy];
+  a.op_mode = 1;
+  if (in != out) CK(cudaMemcpyAsync(out, in, sizeof(double2) * g.d * g.N, cudaMemcpyDeviceToDevice, s));
+  Scratch sc;
+  if (sc.alloc(a, R.num_sms, s)) return 1;
+  Launcher Lc{s, R.num_sms};
+  int rc = run_axis(Lc, a, g, 0, false, 1.0);
+  if (!rc && g.d == 3) rc = run_axis(Lc, a, g, 1, false, 1.0);
+  if (!rc) {
+    ColGeom mid{};
+    const KInfo* kmid;
+    if (g.d == 2) {
+      mid.axis = 1;
+      mid.nouter = 1;
+      mid.stride = g.nx;
+      mid.nstrips = (int)(g.nx / R.tab[g.lgy].col_w);
+      kmid = &R.tab[g.lgy].col[KC_MID2_BASIC];
+    } else {
+      mid.axis = 2;
+      mid.nouter = (int)g.ny;
+      mid.stride = g.nx * g.ny;
+      mid.ostride = g.nx;
+      mid.nstrips = (int)(g.nx / R.tab[g.lgz].col3_w);
+      kmid = &R.tab[g.lgz].col[KC_MID3_BASIC];
+    }
+    void* args[] = {&a, &mid};
+    rc = Lc.go(*kmid, (long long)mid.nouter * mid.nstrips, args);
+  }
+  if (!rc && g.d == 3) rc = run_axis(Lc, a, g, 1, true, 1.0);
+  if (!rc) rc = run_axis(Lc, a, g, 0, true, a.inv_n);
+  g_launches += Lc.count;
+  if (rc) return rc;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// test hook: run only the projection sweep (line FFT, Gamma, inverse line
+// FFT along y in 2-D / z in 3-D) on a field already transformed along the
+// other axes.
+int fftc_debug_project(const fftc_problem* pb, void* data, void* stream) {
+  g_err.clear();
+  GridInfo g;
+  if (int rc = grid_info(pb, g)) return rc;
+  if (ensure_registry()) return 1;
+  Registry& R = reg();
+  cudaStream_t s = (cudaStream_t)stream;
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.d = g.d;
+  a.nx = (int)g.nx;
+  a.ny = (int)g.ny;
+  a.nz = (int)g.nz;
+  a.N = g.N;
+  a.inv_n = 1.0 / (double)g.N;
+  a.gscale = 1.0;
+  a.A = a.B = (double2*)data;
+  a.op_mode = 1;
+  a.tw[0] = R.tw[g.lgx];
+  a.tw[1] = R.tw[g.lgy];
+  a.tw[2] = g.d == 3 ? R.tw[g.lgz] : R.tw[g.lgy];
+  Scratch sc;
+  if (sc.alloc(a, R.num_sms, s)) return 1;
+  Launcher Lc{s, R.num_sms};
+  ColGeom mid{};
+  const KInfo* kmid;
+  if (g.d == 2) {
+    mid.axis = 1;
+    mid.nouter = 1;
+    mid.stride = g.nx;
+    mid.nstrips = (int)(g.nx / R.tab[g.lgy].col_w);
+    kmid = &R.tab[g.lgy].col[KC_MID2_BASIC];
+  } else {
+    mid.axis = 2;
+    mid.nouter = (int)g.ny;
+    mid.stride = g.nx * g.ny;
+    mid.ostride = g.nx;
+    mid.nstrips = (int)(g.nx / R.tab[g.lgz].col3_w);
+    kmid = &R.tab[g.lgz].col[KC_MID3_BASIC];
+  }
+  void* args[] = {&a, &mid};
+  if (int rc = Lc.go(*kmid, (long long)mid.nouter * mid.nstrips, args)) return rc;
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fftc_solve_host(const fftc_problem* pb, const fftc_params* pr, double* history, int64_t history_cap,
+                    void* E_host, void* J_host, void* aug_host, fftc_result* out) {
+  g_err.clear();
+  if (!pb || !pb->chi) {
+    g_err = "null problem";
+    return 2;
+  }
+  const long long N = pb->n[0] * pb->n[1] * (pb->d == 3 ? pb->n[2] : 1);
+  const size_t fld = sizeof(double2) * (size_t)pb->d * N;
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint8_t* chi = nullptr;
+  void *E = nullptr, *J = nullptr, *aug = nullptr;
+  int rc = 0;
+  do {
+    if (cudaMallocAsync((void**)&chi, N, s) != cudaSuccess) { rc = 1; break; }
+    if (cudaMemcpyAsync(chi, pb->chi, N, cudaMemcpyHostToDevice, s) != cudaSuccess) { rc = 1; break; }
+    if (E_host && cudaMallocAsync(&E, fld, s) != cudaSuccess) { rc = 1; break; }
+    if (J_host && cudaMallocAsync(&J, fld, s) != cudaSuccess) { rc = 1; break; }
+    if (aug_host && cudaMallocAsync(&aug, 3 * fld, s) != cudaSuccess) { rc = 1; break; }
+    fftc_problem p2 = *pb;
+    p2.chi = chi;
+    rc = fftc_solve(&p2, pr, history, history_cap, E, J, aug, out, s);
+    if (rc) break;
+    if (E_host && cudaMemcpyAsync(E_host, E, fld, cudaMemcpyDeviceToHost, s) != cudaSuccess) { rc = 1; break; }
+    if (J_host && cudaMemcpyAsync(J_host, J, fld, cudaMemcpyDeviceToHost, s) != cudaSuccess) { rc = 1; break; }
+    if (aug_host && cudaMemcpyAsync(aug_host, aug, 3 * fld, cudaMemcpyDeviceToHost, s) != cudaSuccess) { rc = 1; break; }
+    if (cudaStreamSynchronize(s) != cudaSuccess) { rc = 1; break; }
+  } while (0);
+  if (rc == 1 && g_err.empty()) g_err = cudaGetErrorString(cudaGetLastError());
+  if (chi) cudaFreeAsync(chi, s);
+  if (E) cudaFreeAsync(E, s);
+  if (J) cudaFreeAsync(J, s);
+  if (aug) cudaFreeAsync(aug, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// instantiate.cuh -- instantiate every sweep kernel for one axis length
+// L = 2^FFTC_LG and register it.  Included by the generated inst_<lg>.cu
+// files so the ~170 kernels compile in parallel translation units.
+#include "sweeps.cuh"
+#include "kernel_table.h"
+
+#ifndef FFTC_LG
+#error "define FFTC_LG before including instantiate.cuh"
+#endif
+
+namespace fftc {
+namespace inst_detail {
+
+constexpr int L = 1 << FFTC_LG;
+// rows: radix-8 lines, at least 64 threads per CTA
+constexpr int E_ROW = L >= 8 ? 8 : L;
+constexpr int T_ROW = L / E_ROW;
+constexpr int G_ROW = T_ROW >= 64 ? 1 : 64 / T_ROW;
+// columns: radix-8, strips of 2 columns (32-B sectors); 1 column at 4096
+constexpr int E_COL = L >= 8 ? 8 : L;
+constexpr int T_COL = L / E_COL;
+constexpr int W2 = L >= 4096 ? 1 : 2;
+constexpr int G2 = (T_COL * W2) >= 64 ? 1 : 64 / (T_COL * W2);
+constexpr int W3 = L >= 2048 ? 1 : 2;
+constexpr int G3 = (T_COL * W3) >= 64 ? 1 : 64 / (T_COL * W3);
+constexpr int WP = 2;  // plain 3-D y passes
+constexpr int GP = (T_COL * WP) >= 64 ? 1 : 64 / (T_COL * WP);
+
+template <int C, int W, int G>
+constexpr int col_smem() {
+  using P = Plan<L, E_COL>;
+  constexpr int SKEW = (W > 1) ? 8 / W : 0;
+  return G * C * W * (P::LP + SKEW) * (int)sizeof(double2);
+}
+template <int C, int G>
+constexpr int row_smem() {
+  return G * C * Plan<L, E_ROW>::LP * (int)sizeof(double2);
+}
+
+template <class K>
+inline KInfo make(K* fn, int threads, int smem, int lines) {
+  KInfo k;
+  k.fn = (const void*)fn;
+  k.threads = threads;
+  k.smem = smem;
+  k.lines = lines;
+  return k;
+}
+
+}  // namespace inst_detail
+}  // namespace fftc
+
+#define FFTC_CAT2(a, b) a##b
+#define FFTC_CAT(a, b) FFTC_CAT2(a, b)
+
+void FFTC_CAT(fftc_fill_table_, FFTC_LG)(fftc::LTable& t) {
+  using namespace fftc;
+  using namespace fftc::inst_detail;
+  t.L = L;
+  t.col_w = W2;
+  t.col3_w = W3;
+  const int trow = G_ROW * T_ROW;
+  t.s1[BASIC] = make(k_sweep1<BASIC, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.s1[EM] = make(k_sweep1<EM, L, E_ROW, G_ROW>, trow, row_smem<2, G_ROW>(), G_ROW);
+  t.s1[BASIC_SUB] = make(k_sweep1<BASIC_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.s1[EM_SUB] = make(k_sweep1<EM_SUB, L, E_ROW, G_ROW>, trow, row_smem<2, G_ROW>(), G_ROW);
+  t.s3[BASIC] = make(k_sweep3<BASIC, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.s3[EM] = make(k_sweep3<EM, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.s3[BASIC_SUB] = make(k_sweep3<BASIC_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.s3[EM_SUB] = make(k_sweep3<EM_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.row_fwd = make(k_row_plain<false, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.row_inv = make(k_row_plain<true, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  t.col[KC_MID2_BASIC] = make(k_col<MID_BASIC, L, E_COL, W2, 2, G2>, G2 * W2 * T_COL, col_smem<2, W2, G2>(), G2);
+  t.col[KC_MID2_EM] = make(k_col<MID_EM, L, E_COL, W2, 2, G2>, G2 * W2 * T_COL, col_smem<2, W2, G2>(), G2);
+  t.col[KC_MID3_BASIC] = make(k_col<MID_BASIC, L, E_COL, W3, 3, G3>, G3 * W3 * T_COL, col_smem<3, W3, G3>(), G3);
+  t.col[KC_MID3_EM] = make(k_col<MID_EM, L, E_COL, W3, 3, G3>, G3 * W3 * T_COL, col_smem<3, W3, G3>(), G3);
+  t.col[KC_FWD] = make(k_col<COL_FWD, L, E_COL, WP, 1, GP>, GP * WP * T_COL, col_smem<1, WP, GP>(), GP);
+  t.col[KC_INV] = make(k_col<COL_INV, L, E_COL, WP, 1, GP>, GP * WP * T_COL, col_smem<1, WP, GP>(), GP);
+}

@@ -1,0 +1,45 @@
+// kernel_table.h -- per-length kernel registry shared by the instantiation
+// units (inst_<lg>.cu) and the host driver (abi.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace fftc {
+
+struct KInfo {
+  const void* fn = nullptr;
+  int threads = 0;     // block size
+  int smem = 0;        // dynamic shared memory (bytes)
+  int lines = 0;       // lines processed per CTA per loop trip (G)
+  int max_active = 0;  // resident CTAs per SM (filled at first use)
+};
+
+// column kernel variants
+enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_FWD = 4, KC_INV = 5, KC_COUNT = 6 };
+
+struct LTable {
+  int L = 0;
+  int col_w = 0;       // strip width of the column kernels (2-D mid / plain)
+  int col3_w = 0;      // strip width of the 3-D mid kernels
+  KInfo s1[4];         // sweep 1 per scheme
+  KInfo s3[4];         // sweep 3 per scheme
+  KInfo col[KC_COUNT];
+  KInfo row_fwd, row_inv;  // plain row transforms (operator API)
+};
+
+constexpr int MAX_LG = 12;  // supported axis lengths 2 .. 4096
+
+}  // namespace fftc
+
+#define FFTC_DECLARE_FILL(LG) void fftc_fill_table_##LG(fftc::LTable& t);
+FFTC_DECLARE_FILL(1)
+FFTC_DECLARE_FILL(2)
+FFTC_DECLARE_FILL(3)
+FFTC_DECLARE_FILL(4)
+FFTC_DECLARE_FILL(5)
+FFTC_DECLARE_FILL(6)
+FFTC_DECLARE_FILL(7)
+FFTC_DECLARE_FILL(8)
+FFTC_DECLARE_FILL(9)
+FFTC_DECLARE_FILL(10)
+FFTC_DECLARE_FILL(11)
+FFTC_DECLARE_FILL(12)

@@ -1,0 +1,733 @@
+// sweeps.cuh -- the fused per-iteration sweeps of the FFT field iteration.
+//
+// One reference iteration (solvers.py:300-321 for basic/em, :395-432 for
+// basic_sub/em_sub) becomes, on a 2-D grid, three kernels:
+//
+//   sweep 1 (rows, x-FFT):   prologue = the pointwise update that produces
+//                            the fields to transform (j = sigma e, or the
+//                            augmented flux Jq and the EM residual field R),
+//                            reductions <j> (and sum |Js|^2 chi), x-FFT.
+//   sweep 2 (columns):       y-FFT, Gamma_1 projection k k^T/|k|^2 in
+//                            registers (spectral_ops.py:120-128), residual by
+//                            Parseval, y-iFFT of the field the update needs;
+//                            the last CTA runs the stopping monitor
+//                            (solvers.py:243-277) on device.
+//   sweep 3 (rows, x-iFFT):  epilogue = the state update for iteration k+1
+//                            and the reduction <Q_raw> / <e_raw> that gives
+//                            the next mean-field pin delta (solvers.py:309,416).
+//
+// On a 3-D grid the y pass and y^-1 pass are separate column sweeps and the
+// Gamma projection moves to the z pass.  All reductions are deterministic:
+// fixed per-thread order, shuffle trees, per-CTA partials and a last-CTA
+// fixed-order combine (no floating-point atomics).
+#pragma once
+#include "fft_engine.cuh"
+
+namespace fftc {
+
+enum SchemeId { BASIC = 0, EM = 1, BASIC_SUB = 2, EM_SUB = 3 };
+enum StatusId { ST_CONVERGED = 0, ST_MAXITERS = 1, ST_DIVERGED = 2 };
+
+constexpr double DIVERGENCE_FACTOR = 1e6;  // solvers.py:50
+constexpr double TINY = 1e-300;            // solvers.py:51
+constexpr int NQMAX = 8;                   // reduction slots per CTA
+
+struct DevState {
+  int stopped;
+  int status;
+  int degenerate;
+  int nrec;          // records written so far (== iterations)
+  long long k;       // index of the iteration being executed (1-based)
+  int has_prev;
+  int pad0;
+  double res0;
+  double2 prev_sstar;
+  double2 last_sstar;  // sigma* of the last evaluated iteration (recorded or not)
+  double2 delta[3];    // mean-field pin of the current iterate
+  double2 jmean[3];    // <j> / <Jq> of the current iterate
+  double js2;          // sum |Js|^2 chi
+  double parseval;     // sum_k |Gamma j^|^2
+  double2 meanE[3];
+  double2 meanJ[3];
+  unsigned int counter;  // last-CTA detection
+  unsigned int pad1;
+};
+
+struct Args {
+  int d, nx, ny, nz;
+  long long N;
+  const uint8_t* chi;
+  double2* X[3];  // state slots: e_raw | Q_raw, S_raw, T_raw
+  double2* A;     // work field 0 (d*N)
+  double2* B;     // work field 1 (d*N)
+  double2* outE;  // finalize targets (nullable)
+  double2* outJ;
+  double2* outAug;  // (3, d, grid)
+  double* partials;
+  double* history;  // [hist_cap][3]
+  int hist_cap;
+  int op_mode;  // 1: operator API call -- no stop flag, no monitor
+  DevState* st;
+  const double2* tw[3];  // twiddles for n_x, n_y, n_z
+  // scalars (host-prepared, see abi.cu)
+  double2 sigma1, s0, e0[3];
+  double e0sq, tol, inv_n, gscale;
+  long long max_iters;
+  double2 inv_s0;                  // 1/s0
+  double2 inv_sum1, inv_sum2;      // 1/(sigma1+s0), 1/(1+s0)
+  double2 sum1, sum2;              // sigma1+s0, 1+s0
+  double2 sm1, sm2;                // sigma1-s0, 1-s0
+  double2 two_s0_e0[3];            // (2 s0) e0_c
+  double2 p1, p2, p3;
+  double2 tm1p1, tm1p2, tm1p3;     // (t-1) p_i
+  double2 cq, cs;                  // p1*((t-1)p1), p2*((t-1)p1)
+  double2 sinv;                    // 1/(1+s0)
+  double2 cinv_p1, cinv_p2, cinv_p3;  // ((t-1)/(t+s0)) p_i
+};
+
+// ----------------------------------------------------------------------------
+// deterministic block reduction + last-CTA combine
+// ----------------------------------------------------------------------------
+template <int NQ>
+__device__ __forceinline__ void warp_sum(double (&acc)[NQ]) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_down_sync(0xffffffffu, acc[q], o);
+}
+
+// Reduce acc over the CTA, write the CTA partial, and return true in the
+// last CTA to finish, with `tot` holding the grid total (fixed order).
+template <int NQ>
+__device__ bool grid_reduce(double (&acc)[NQ], double (&tot)[NQ], const Args& a) {
+  __shared__ double red[32][NQ];
+  __shared__ int am_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  warp_sum<NQ>(acc);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) red[warp][q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) s[q] = 0.0;
+    for (int w = 0; w < nw; ++w)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) s[q] += red[w][q];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) a.partials[(size_t)blockIdx.x * NQ + q] = s[q];
+    __threadfence();
+    unsigned prev = atomicAdd(&a.st->counter, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  double s[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) s[q] = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) s[q] += __ldcg(&a.partials[(size_t)b * NQ + q]);
+  warp_sum<NQ>(s);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) red[warp][q] = s[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) tot[q] = 0.0;
+  for (int w = 0; w < nw; ++w)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tot[q] += red[w][q];
+  if (threadIdx.x == 0) a.st->counter = 0;
+  return true;
+}
+
+// accumulate complex v into slot pair (2c, 2c+1) with a runtime component c
+template <int NQ>
+__device__ __forceinline__ void acc_c(double (&acc)[NQ], int c, double2 v) {
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc)
+    if (2 * cc + 1 < NQ && c == cc) {
+      acc[2 * cc] += v.x;
+      acc[2 * cc + 1] += v.y;
+    }
+}
+
+// ----------------------------------------------------------------------------
+// pointwise algebra shared by the sweeps (reference formulas)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double2 sigma_at(const Args& a, bool in1) {
+  return in1 ? a.sigma1 : make_double2(1.0, 0.0);
+}
+
+// augmented local operator A (solvers.py:355-363) on one pixel/component
+struct AugFlux {
+  double2 jq, js, jt;
+};
+__device__ __forceinline__ AugFlux apply_A(const Args& a, bool in1, double2 q, double2 s, double2 t) {
+  AugFlux f;
+  if (in1) {
+    double2 u = cadd(cadd(cmul(a.p1, q), cmul(a.p2, s)), cmul(a.p3, t));
+    f.jq = cadd(cmul(a.tm1p1, u), q);
+    f.js = cadd(cmul(a.tm1p2, u), s);
+    f.jt = cadd(cmul(a.tm1p3, u), t);
+  } else {
+    f.jq = q;  // u = 0: (t-1) p1 * 0 + q
+    f.js = czero();
+    f.jt = czero();
+  }
+  return f;
+}
+
+// (A + s0 I)^{-1} W update of em_sub (solvers.py:408-411)
+__device__ __forceinline__ void em_sub_update(const Args& a, bool in1, double2 wq, double2 ws, double2 wt,
+                                              double2& q, double2& s, double2& t) {
+  if (in1) {
+    double2 u = cadd(cadd(cmul(a.p1, wq), cmul(a.p2, ws)), cmul(a.p3, wt));
+    q = cmul(a.sinv, csub(wq, cmul(a.cinv_p1, u)));
+    s = cmul(a.sinv, csub(ws, cmul(a.cinv_p2, u)));
+    t = cmul(a.sinv, csub(wt, cmul(a.cinv_p3, u)));
+  } else {
+    q = cmul(a.sinv, wq);
+    s = czero();
+    t = czero();
+  }
+}
+
+// Jq, Js of the pinned iterate (solvers.py:419-420)
+__device__ __forceinline__ void pinned_flux(const Args& a, bool in1, double2 jq_raw, double2 js_raw, double2 dl,
+                                            double2& jq, double2& js) {
+  if (in1) {
+    jq = cadd(cadd(jq_raw, cmul(a.cq, dl)), dl);
+    js = cadd(js_raw, cmul(a.cs, dl));
+  } else {
+    jq = cadd(jq_raw, dl);
+    js = js_raw;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// stopping monitor (solvers.py:243-277), one thread
+// ----------------------------------------------------------------------------
+static __device__ __noinline__ void monitor_step(const Args& a, double total_sq) {
+  DevState* st = a.st;
+  double2 jm[3];
+  double den2 = 0.0;
+  double2 s = czero();
+  for (int c = 0; c < a.d; ++c) {
+    jm[c] = st->jmean[c];
+    den2 += cabs2(jm[c]);
+    // np.vdot(e0, jmean): conj(e0) . jmean
+    double2 e = a.e0[c];
+    s = cadd(s, make_double2(e.x * jm[c].x + e.y * jm[c].y, e.x * jm[c].y - e.y * jm[c].x));
+  }
+  const double den = sqrt(den2);
+  const double2 sstar = make_double2(s.x / a.e0sq, s.y / a.e0sq);
+  st->last_sstar = sstar;
+  if (den < TINY && isfinite(den)) {  // solvers.py:315-317 / :424-426
+    st->degenerate = 1;
+    st->status = ST_DIVERGED;
+    st->stopped = 1;
+    return;
+  }
+  const double res = sqrt(total_sq * a.inv_n) / den;
+  if (!(isfinite(res) && isfinite(sstar.x) && isfinite(sstar.y))) {  // :256-260
+    st->status = ST_DIVERGED;
+    st->stopped = 1;
+    return;
+  }
+  const int slot = st->nrec % a.hist_cap;
+  a.history[3 * slot + 0] = sstar.x;
+  a.history[3 * slot + 1] = sstar.y;
+  a.history[3 * slot + 2] = res;
+  st->nrec += 1;
+  if (st->nrec == 1) st->res0 = res;
+  bool settled = true;
+  if (st->has_prev) {
+    double2 dlt = csub(sstar, st->prev_sstar);
+    settled = hypot(dlt.x, dlt.y) <= a.tol * hypot(sstar.x, sstar.y);
+  }
+  if (res <= a.tol && settled) {
+    st->status = ST_CONVERGED;
+    st->stopped = 1;
+    return;
+  }
+  if (st->res0 > 0.0 && res > DIVERGENCE_FACTOR * st->res0) {
+    st->status = ST_DIVERGED;
+    st->stopped = 1;
+    return;
+  }
+  st->prev_sstar = sstar;
+  st->has_prev = 1;
+  if (st->k >= a.max_iters) {  // loop exhausted: status stays MaxIters
+    st->stopped = 1;
+    return;
+  }
+  st->k += 1;
+}
+
+// ----------------------------------------------------------------------------
+// shared memory buffer accessor for fft_line
+// ----------------------------------------------------------------------------
+struct SmemBuf {
+  double2* base;
+  int stride;  // distance between channel buffers (double2 units)
+  __device__ __forceinline__ double2* operator()(int c) const { return base + c * stride; }
+};
+struct SyncAll {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// ============================================================================
+// sweep 1: rows (x-pass), forward.  Line = (component c, row r); a CTA runs
+// G lines at a time (one per thread group of T = L/E threads).
+// ============================================================================
+template <int S>
+struct Sweep1Traits;
+template <>
+struct Sweep1Traits<BASIC> { static constexpr int C = 1; static constexpr int NQ = 6; };
+template <>
+struct Sweep1Traits<EM> { static constexpr int C = 2; static constexpr int NQ = 6; };
+template <>
+struct Sweep1Traits<BASIC_SUB> { static constexpr int C = 1; static constexpr int NQ = 7; };
+template <>
+struct Sweep1Traits<EM_SUB> { static constexpr int C = 2; static constexpr int NQ = 7; };
+
+template <int S, int L, int E, int G>
+__global__ void __launch_bounds__(G*(L / E)) k_sweep1(Args a) {
+  using P = Plan<L, E>;
+  constexpr int C = Sweep1Traits<S>::C;
+  constexpr int NQ = Sweep1Traits<S>::NQ;
+  constexpr int T = P::T;
+  extern __shared__ double2 smem[];
+  if (a.st->stopped) return;
+  const int t = threadIdx.x % T, g = threadIdx.x / T;
+  const long long rows = (long long)a.ny * a.nz;
+  const long long lines = rows * a.d;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  SmemBuf buf{smem + g * C * P::LP, P::LP};
+  for (long long line0 = (long long)blockIdx.x * G; line0 < lines; line0 += (long long)gridDim.x * G) {
+    const long long line = line0 + g;
+    const bool live = line < lines;
+    const int c = live ? (int)(line / rows) : 0;
+    const long long row = live ? line - (long long)c * rows : 0;
+    const size_t off = (size_t)c * a.N + (size_t)row * L;
+    const uint8_t* chi = a.chi + (size_t)row * L;
+    const double2 dl = a.st->delta[c];
+    double2 v[C][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int x = pos_first<L, E>(false, t, i);
+      if (!live) {
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) v[cc][i] = czero();
+        continue;
+      }
+      const bool in1 = chi[x] != 0;
+      if constexpr (S == BASIC) {
+        double2 e = cadd(a.X[0][off + x], dl);
+        double2 j = cmul(sigma_at(a, in1), e);  // j = sigma e  (solvers.py:310-311)
+        v[0][i] = j;
+        acc_c<NQ>(acc, c, j);
+      } else if constexpr (S == EM) {
+        double2 er = a.X[0][off + x];
+        v[0][i] = cmul(in1 ? a.sm1 : a.sm2, er);           // r = (sigma - s0) e_raw  (:303)
+        double2 j = cmul(sigma_at(a, in1), cadd(er, dl));  // j = sigma (e_raw + delta)
+        v[1][i] = j;
+        acc_c<NQ>(acc, c, j);
+      } else {
+        double2 q = a.X[0][off + x];
+        double2 s = in1 ? a.X[1][off + x] : czero();
+        double2 tt = czero();
+        if constexpr (S == EM_SUB) tt = in1 ? a.X[2][off + x] : czero();
+        AugFlux f = apply_A(a, in1, q, s, tt);  // (:412)
+        double2 jq, js;
+        pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
+        if constexpr (S == EM_SUB) {
+          v[0][i] = csub(f.jq, cmul(a.s0, q));  // Rq = Jq_raw - s0 Q_raw  (:398)
+          v[1][i] = jq;
+        } else {
+          v[0][i] = jq;
+        }
+        acc_c<NQ>(acc, c, jq);
+        if (in1) acc[6] += cabs2(js);  // sum |Js|^2 chi  (:429)
+      }
+    }
+    fft_line<L, E, C, false>(v, t, a.tw[0], buf, SyncAll{});
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int x = pos_last<L, E>(false, t, i);
+        a.A[off + x] = v[0][i];
+        if constexpr (C == 2) a.B[off + x] = v[C - 1][i];
+      }
+    }
+  }
+  double tot[NQ];
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0) {
+    for (int c = 0; c < a.d; ++c) a.st->jmean[c] = make_double2(tot[2 * c] * a.inv_n, tot[2 * c + 1] * a.inv_n);
+    if constexpr (NQ > 6) a.st->js2 = tot[NQ - 1];
+    else a.st->js2 = 0.0;
+  }
+}
+
+// ============================================================================
+// sweep 3: rows (x-pass), inverse + state update.  Line = (c, row).
+// ============================================================================
+template <int S, int L, int E, int G>
+__global__ void __launch_bounds__(G*(L / E)) k_sweep3(Args a) {
+  using P = Plan<L, E>;
+  constexpr int NQ = 6;
+  constexpr int T = P::T;
+  extern __shared__ double2 smem[];
+  if (a.st->stopped) return;
+  const int t = threadIdx.x % T, g = threadIdx.x / T;
+  const long long rows = (long long)a.ny * a.nz;
+  const long long lines = rows * a.d;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  SmemBuf buf{smem + g * P::LP, P::LP};
+  for (long long line0 = (long long)blockIdx.x * G; line0 < lines; line0 += (long long)gridDim.x * G) {
+    const long long line = line0 + g;
+    const bool live = line < lines;
+    const int c = live ? (int)(line / rows) : 0;
+    const long long row = live ? line - (long long)c * rows : 0;
+    const size_t off = (size_t)c * a.N + (size_t)row * L;
+    const uint8_t* chi = a.chi + (size_t)row * L;
+    const double2 dl = a.st->delta[c];
+    double2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[0][i] = live ? a.A[off + pos_first<L, E>(true, t, i)] : czero();
+    fft_line<L, E, 1, true>(v, t, a.tw[0], buf, SyncAll{});
+    if (!live) continue;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int x = pos_last<L, E>(true, t, i);
+      const bool in1 = chi[x] != 0;
+      const double2 gq = cscale(v[0][i], a.inv_n);  // ifft normalisation 1/N
+      double2 qn;
+      if constexpr (S == BASIC) {
+        // e_raw <- (e_raw + delta) - g / s0      (solvers.py:306)
+        qn = csub(cadd(a.X[0][off + x], dl), cmul(gq, a.inv_s0));
+        a.X[0][off + x] = qn;
+      } else if constexpr (S == EM) {
+        // w = 2 s0 e0 + (I - 2 Gamma) r;  e_raw = w / (sigma + s0)   (:303-308)
+        double2 w = cadd(a.two_s0_e0[c], gq);
+        qn = cmul(w, in1 ? a.inv_sum1 : a.inv_sum2);
+        a.X[0][off + x] = qn;
+      } else if constexpr (S == BASIC_SUB) {
+        // Q_raw <- Q - g/s0 ; S_raw <- chi (S - Js/s0)   (:405-406)
+        double2 q = a.X[0][off + x];
+        qn = csub(cadd(q, dl), cmul(gq, a.inv_s0));
+        a.X[0][off + x] = qn;
+        if (in1) {
+          double2 s = a.X[1][off + x];
+          AugFlux f = apply_A(a, true, q, s, czero());
+          double2 jq, js;
+          pinned_flux(a, true, f.jq, f.js, dl, jq, js);
+          a.X[1][off + x] = csub(s, cmul(js, a.inv_s0));
+        }
+      } else {
+        // em_sub: W from the raw iterate, then (A + s0)^-1 W   (:398-411)
+        double2 wq = cadd(a.two_s0_e0[c], gq);
+        double2 ws = czero(), wt = czero();
+        if (in1) {
+          double2 q = a.X[0][off + x], s = a.X[1][off + x], tt = a.X[2][off + x];
+          AugFlux f = apply_A(a, true, q, s, tt);
+          const double2 rs = csub(f.js, cmul(a.s0, s));  // Rs = Js_raw - s0 S_raw
+          ws = make_double2(-rs.x, -rs.y);
+          wt = csub(f.jt, cmul(a.s0, tt));               // Rt = Jt_raw - s0 T_raw
+        }
+        double2 sn, tn;
+        em_sub_update(a, in1, wq, ws, wt, qn, sn, tn);
+        a.X[0][off + x] = qn;
+        if (in1) {
+          a.X[1][off + x] = sn;
+          a.X[2][off + x] = tn;
+        }
+      }
+      acc_c<NQ>(acc, c, qn);
+    }
+  }
+  double tot[NQ];
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0) {
+    for (int c = 0; c < a.d; ++c) {
+      double2 m = make_double2(tot[2 * c] * a.inv_n, tot[2 * c + 1] * a.inv_n);
+      a.st->delta[c] = csub(a.e0[c], m);  // delta = e0 - <raw>  (:309, :416)
+    }
+  }
+}
+
+// ============================================================================
+// plain row transform (operator API / tests): line = (c, row) of field A,
+// in place, optional scale on output.
+// ============================================================================
+template <bool INV, int L, int E, int G>
+__global__ void __launch_bounds__(G*(L / E)) k_row_plain(Args a, double scale) {
+  using P = Plan<L, E>;
+  constexpr int T = P::T;
+  extern __shared__ double2 smem[];
+  const int t = threadIdx.x % T, g = threadIdx.x / T;
+  const long long lines = (long long)a.ny * a.nz * a.d;
+  SmemBuf buf{smem + g * P::LP, P::LP};
+  for (long long line0 = (long long)blockIdx.x * G; line0 < lines; line0 += (long long)gridDim.x * G) {
+    const long long line = line0 + g;
+    const bool live = line < lines;
+    const size_t off = (size_t)(live ? line : 0) * L;
+    double2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[0][i] = live ? a.A[off + pos_first<L, E>(INV, t, i)] : czero();
+    fft_line<L, E, 1, INV>(v, t, a.tw[0], buf, SyncAll{});
+    if (live)
+#pragma unroll
+      for (int i = 0; i < E; ++i) a.A[off + pos_last<L, E>(INV, t, i)] = cscale(v[0][i], scale);
+  }
+}
+
+// ============================================================================
+// column sweeps.  A "line" is a strip of W adjacent x-columns of one field
+// along an axis with element stride `stride`; the line origin is
+// outer*ostride + strip*W.  A CTA runs G lines at a time.  MODE:
+//   MID_BASIC : fwd, g = Gamma F (Parseval), inv, write back      (basic, basic_sub)
+//   MID_EM    : field 0: fwd, (I - 2 Gamma) F, inv, write back;
+//               field 1: fwd, Parseval of Gamma F only            (em, em_sub)
+//   COL_FWD / COL_INV : plain transform of one component          (3-D y passes)
+// ============================================================================
+enum ColMode { MID_BASIC = 0, MID_EM = 1, COL_FWD = 2, COL_INV = 3 };
+
+struct ColGeom {
+  int axis;           // twiddle table / wave-number axis of the line (1 = y, 2 = z)
+  int nouter;         // outer lines per strip row
+  long long stride;   // element stride along the line
+  long long ostride;  // stride of the outer index
+  int nstrips;        // nx / W
+  int pad;
+};
+
+template <int MODE, int L, int E, int W, int C, int G>
+__global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
+  using P = Plan<L, E>;
+  constexpr int T = P::T;
+  constexpr int NQ = 1;
+  constexpr int SKEW = (W > 1) ? 8 / W : 0;
+  constexpr int CHS = W * (P::LP + SKEW);  // channel stride in shared memory
+  extern __shared__ double2 smem[];
+  if (!a.op_mode && a.st->stopped) return;
+  const int col = threadIdx.x % W, t = (threadIdx.x / W) % T, g = threadIdx.x / (W * T);
+  SmemBuf buf{smem + (size_t)g * C * CHS + col * (P::LP + SKEW), CHS};
+  const int nfields = (MODE == MID_EM) ? 2 : 1;
+  const int ncomp_lines = (C == 1) ? a.d : 1;  // plain passes: one component per line
+  const long long per_field = (long long)gm.nouter * gm.nstrips * ncomp_lines;
+  const long long lines = per_field * nfields;
+  const double2* tw = a.tw[gm.axis];
+  double acc[NQ] = {0.0};
+  for (long long line0 = (long long)blockIdx.x * G; line0 < lines; line0 += (long long)gridDim.x * G) {
+    const long long line = line0 + g;
+    const bool live = line < lines;
+    const int f = live ? (int)(line / per_field) : 0;
+    long long rem = live ? line - (long long)f * per_field : 0;
+    const int cl = (int)(rem / ((long long)gm.nouter * gm.nstrips));
+    rem -= (long long)cl * gm.nouter * gm.nstrips;
+    const int outer = (int)(rem / gm.nstrips);
+    const int strip = (int)(rem - (long long)outer * gm.nstrips);
+    const int x = strip * W + col;
+    double2* F = (f == 0) ? a.A : a.B;
+    const size_t base = (size_t)outer * gm.ostride + x;
+    double2 v[C][E];
+    if constexpr (MODE == COL_INV) {
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        v[0][i] = live ? F[(size_t)cl * a.N + base + (size_t)pos_first<L, E>(true, t, i) * gm.stride] : czero();
+      fft_line<L, E, 1, true>(v, t, tw, buf, SyncAll{});
+      if (live)
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          F[(size_t)cl * a.N + base + (size_t)pos_last<L, E>(true, t, i) * gm.stride] = v[0][i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const size_t p = base + (size_t)pos_first<L, E>(false, t, i) * gm.stride;
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c][i] = live ? F[(size_t)(C == 1 ? cl : c) * a.N + p] : czero();
+      }
+      fft_line<L, E, C, false>(v, t, tw, buf, SyncAll{});
+      if constexpr (MODE == COL_FWD) {
+        if (live)
+#pragma unroll
+          for (int i = 0; i < E; ++i)
+            F[(size_t)cl * a.N + base + (size_t)pos_last<L, E>(false, t, i) * gm.stride] = v[0][i];
+      } else {
+        // Gamma projection in registers (spectral_ops.py:124-127).  Wave
+        // numbers: x from the column, the line axis from the position, the
+        // remaining axis (3-D) from the outer index.
+        const double kx = (double)wavenum(x, a.nx);
+        double kyo = 0.0;
+        if constexpr (C == 3) kyo = (double)wavenum(outer, a.ny);
+        const bool parseval_only = (MODE == MID_EM) && f == 1;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int pos = pos_last<L, E>(false, t, i);
+          double k[3];
+          k[0] = kx;
+          if constexpr (C == 2) {
+            k[1] = (double)wavenum(pos, a.ny);
+            k[2] = 0.0;
+          } else {
+            k[1] = kyo;
+            k[2] = (double)wavenum(pos, a.nz);
+          }
+          double k2 = k[0] * k[0];
+#pragma unroll
+          for (int c = 1; c < C; ++c) k2 += k[c] * k[c];
+          const double ik2 = (k2 != 0.0) ? (1.0 / k2) * a.gscale : 0.0;
+          double2 dot = cscale(v[0][i], k[0]);
+#pragma unroll
+          for (int c = 1; c < C; ++c) dot = cadd(dot, cscale(v[c][i], k[c]));
+          dot = cscale(dot, ik2);
+          if (MODE == MID_BASIC || parseval_only) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              const double2 gc = cscale(dot, k[c]);
+              // Parseval: sum_x |g|^2 = N sum_k |g^/N|^2; square the 1/N-scaled
+              // mode so the sum overflows no earlier than the reference's
+              if (live) acc[0] += cabs2(cscale(gc, a.inv_n));
+              v[c][i] = gc;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < C; ++c) v[c][i] = csub(v[c][i], cscale(dot, 2.0 * k[c]));
+          }
+        }
+        // Parseval-only lines need no inverse; skip it when the whole CTA agrees
+        if (MODE == MID_EM && __syncthreads_and(parseval_only || !live)) continue;
+        fft_line<L, E, C, true>(v, t, tw, buf, SyncAll{});
+        if (live && !parseval_only) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const size_t p = base + (size_t)pos_last<L, E>(true, t, i) * gm.stride;
+#pragma unroll
+            for (int c = 0; c < C; ++c) F[(size_t)c * a.N + p] = v[c][i];
+          }
+        }
+      }
+    }
+  }
+  if constexpr (MODE == MID_BASIC || MODE == MID_EM) {
+    double tot[NQ];
+    if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
+      monitor_step(a, tot[0] * (double)a.N + a.st->js2);
+  }
+}
+
+// ============================================================================
+// init and finalize (elementwise over component-major d*N)
+// ============================================================================
+template <int S>
+__global__ void __launch_bounds__(256) k_init(Args a) {
+  constexpr int NQ = 6;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  const long long total = (long long)a.d * a.N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / a.N);
+    const long long p = i - (long long)c * a.N;
+    const bool in1 = a.chi[p] != 0;
+    const double2 e0 = a.e0[c];
+    double2 q;
+    if constexpr (S == BASIC) {
+      q = e0;
+    } else if constexpr (S == EM) {
+      double2 w = cmul(in1 ? a.sum1 : a.sum2, e0);  // w = (sigma + s0) e0   (:294)
+      q = cmul(w, in1 ? a.inv_sum1 : a.inv_sum2);   // e_raw = w/(sigma+s0) (:308)
+    } else if constexpr (S == BASIC_SUB) {
+      q = e0;
+      a.X[1][i] = czero();
+    } else {
+      // W = A F + s0 F with F = (e0, 0, 0)   (:386-387), then (A+s0)^-1 W
+      AugFlux f = apply_A(a, in1, e0, czero(), czero());
+      double2 wq = cadd(f.jq, cmul(a.s0, e0));
+      double2 ws = f.js, wt = f.jt;
+      double2 sn, tn;
+      em_sub_update(a, in1, wq, ws, wt, q, sn, tn);
+      a.X[1][i] = sn;
+      a.X[2][i] = tn;
+    }
+    a.X[0][i] = q;
+    acc_c<NQ>(acc, c, q);
+  }
+  double tot[NQ];
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0) {
+    DevState* st = a.st;
+    for (int c = 0; c < a.d; ++c) {
+      double2 m = make_double2(tot[2 * c] * a.inv_n, tot[2 * c + 1] * a.inv_n);
+      st->delta[c] = csub(a.e0[c], m);
+    }
+    st->stopped = 0;
+    st->status = ST_MAXITERS;
+    st->degenerate = 0;
+    st->nrec = 0;
+    st->k = 1;
+    st->has_prev = 0;
+    st->res0 = 0.0;
+    st->last_sstar = czero();
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) k_finalize(Args a) {
+  constexpr int NQ = 12;  // meanE (6) + meanJ (6)
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  const long long total = (long long)a.d * a.N;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / a.N);
+    const long long p = i - (long long)c * a.N;
+    const bool in1 = a.chi[p] != 0;
+    const double2 dl = a.st->delta[c];
+    double2 E, J;
+    if constexpr (S == BASIC || S == EM) {
+      E = cadd(a.X[0][i], dl);
+      J = cmul(sigma_at(a, in1), E);
+    } else {
+      double2 q = a.X[0][i];
+      double2 s = in1 ? a.X[1][i] : czero();
+      double2 tt = (S == EM_SUB && in1) ? a.X[2][i] : czero();
+      AugFlux f = apply_A(a, in1, q, s, tt);
+      double2 js;
+      pinned_flux(a, in1, f.jq, f.js, dl, J, js);
+      E = cadd(q, dl);
+      if (a.outAug) {
+        a.outAug[i] = E;
+        a.outAug[total + i] = s;
+        a.outAug[2 * total + i] = tt;
+      }
+    }
+    if (a.outE) a.outE[i] = E;
+    if (a.outJ) a.outJ[i] = J;
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc)
+      if (c == cc) {
+        acc[2 * cc] += E.x;
+        acc[2 * cc + 1] += E.y;
+        acc[6 + 2 * cc] += J.x;
+        acc[6 + 2 * cc + 1] += J.y;
+      }
+  }
+  double tot[NQ];
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0) {
+    for (int c = 0; c < a.d; ++c) {
+      a.st->meanE[c] = make_double2(tot[2 * c] * a.inv_n, tot[2 * c + 1] * a.inv_n);
+      a.st->meanJ[c] = make_double2(tot[6 + 2 * c] * a.inv_n, tot[6 + 2 * c + 1] * a.inv_n);
+    }
+  }
+}
+
+}  // namespace fftc

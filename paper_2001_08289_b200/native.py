@@ -1,0 +1,95 @@
+"""ctypes binding of the C ABI declared in ``include/fftcond_b200.h``.
+
+The product path has no CPU fallback: if ``libfftcond_b200.so`` is missing
+or does not export the declared symbols, :func:`lib` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfftcond_b200.so")
+
+# every symbol declared in include/fftcond_b200.h
+EXPORTS = (
+    "fftc_solve",
+    "fftc_solve_host",
+    "fftc_supported_length",
+    "fftc_last_error",
+    "fftc_version",
+    "fftc_launch_count",
+    "fftc_fft",
+    "fftc_gamma1",
+)
+
+FFTC_CONVERGED, FFTC_MAX_ITERS, FFTC_DIVERGED = 0, 1, 2
+
+
+class Problem(C.Structure):
+    _fields_ = [("d", C.c_int32), ("reserved", C.c_int32), ("n", C.c_int64 * 3),
+                ("chi", C.c_void_p)]
+
+
+class Params(C.Structure):
+    _fields_ = [("scheme", C.c_int32), ("reserved", C.c_int32),
+                ("sigma1", C.c_double * 2), ("sigma0", C.c_double * 2), ("t", C.c_double * 2),
+                ("p1", C.c_double * 2), ("p2", C.c_double * 2), ("p3", C.c_double * 2),
+                ("e0", (C.c_double * 2) * 3), ("tol", C.c_double), ("max_iters", C.c_int64),
+                ("gamma1_scale", C.c_double)]
+
+
+class Result(C.Structure):
+    _fields_ = [("status", C.c_int32), ("degenerate_flux", C.c_int32), ("iterations", C.c_int64),
+                ("sigma_star", C.c_double * 2), ("mean_E", (C.c_double * 2) * 3),
+                ("mean_J", (C.c_double * 2) * 3), ("kernel_launches", C.c_int64),
+                ("device_ms", C.c_double)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load the CUDA library once; raise loudly if it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: build it with `python -m paper_2001_08289_b200.build_ext` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name in EXPORTS:
+            getattr(L, name)  # AttributeError if missing
+        vp, i64 = C.c_void_p, C.c_int64
+        L.fftc_solve.argtypes = [C.POINTER(Problem), C.POINTER(Params), vp, i64, vp, vp, vp,
+                                 C.POINTER(Result), vp]
+        L.fftc_solve.restype = C.c_int
+        L.fftc_solve_host.argtypes = [C.POINTER(Problem), C.POINTER(Params), vp, i64, vp, vp, vp,
+                                      C.POINTER(Result)]
+        L.fftc_solve_host.restype = C.c_int
+        L.fftc_fft.argtypes = [C.POINTER(Problem), vp, C.c_int32, C.c_int32, vp]
+        L.fftc_fft.restype = C.c_int
+        L.fftc_gamma1.argtypes = [C.POINTER(Problem), vp, vp, C.c_double, vp]
+        L.fftc_gamma1.restype = C.c_int
+        L.fftc_supported_length.argtypes = [i64]
+        L.fftc_supported_length.restype = C.c_int
+        L.fftc_last_error.argtypes = []
+        L.fftc_last_error.restype = C.c_char_p
+        L.fftc_version.restype = C.c_int
+        L.fftc_launch_count.restype = C.c_int64
+        _lib = L
+        return L
+
+
+def last_error() -> str:
+    return lib().fftc_last_error().decode(errors="replace")
+
+
+def cpair(z) -> tuple:
+    z = complex(z)
+    return (z.real, z.imag)

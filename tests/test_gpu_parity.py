@@ -1,0 +1,125 @@
+"""GPU parity: the CUDA iteration (through the public API and the C ABI)
+against golden fixtures frozen from the live reference (2-D) and the
+oracle restatement (3-D).  Protocol in tests/parity.py."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import GOLDEN, load_group
+from parity import check, field_check
+
+pytestmark = pytest.mark.gpu
+
+ALPHA, BETA = 0.25, 4.0
+
+
+def _chi(geom):
+    # same builders as oracle/gen_golden.py (duplicated: the GPU box has no
+    # /root/reference and tests must not depend on the generator's imports)
+    kind = geom["kind"]
+    if kind == "square":
+        n, m = geom["n"], geom["side"]
+        chi = np.zeros((n, n), dtype=bool)
+        lo = (n - m) // 2
+        chi[lo:lo + m, lo:lo + m] = True
+        return chi
+    if kind == "uniform":
+        return np.full((geom["ny"], geom["nx"]), bool(geom["phase1"]))
+    if kind == "laminate_x":
+        chi = np.zeros((geom["n"], geom["n"]), dtype=bool)
+        chi[:, ::2] = True
+        return chi
+    if kind == "laminate_y":
+        chi = np.zeros((geom["n"], geom["n"]), dtype=bool)
+        chi[::2, :] = True
+        return chi
+    if kind == "rect":
+        ny, nx, my, mx = geom["ny"], geom["nx"], geom["my"], geom["mx"]
+        chi = np.zeros((ny, nx), dtype=bool)
+        chi[(ny - my) // 2:(ny - my) // 2 + my, (nx - mx) // 2:(nx - mx) // 2 + mx] = True
+        return chi
+    if kind == "random":
+        rng = np.random.default_rng(geom["seed"])
+        return rng.random((geom["ny"], geom["nx"])) < geom["frac"]
+    if kind == "cube":
+        n, m = geom["n"], geom["side"]
+        chi = np.zeros((n, n, n), dtype=bool)
+        lo = (n - m) // 2
+        chi[lo:lo + m, lo:lo + m, lo:lo + m] = True
+        return chi
+    if kind == "embed2d":
+        return np.repeat(_chi(geom["base"])[None], geom["nz"], axis=0)
+    if kind == "random3d":
+        rng = np.random.default_rng(geom["seed"])
+        return rng.random((geom["n"],) * 3) < geom["frac"]
+    raise ValueError(kind)
+
+
+def run_case(case):
+    import paper_2001_08289_b200 as fb
+
+    chi = _chi(case["geom"])
+    sch = fb.SchemeKind(case["scheme"])
+    kw = dict(scheme=sch, sigma1=complex(*case["sigma1"]), tol=case["tol"], max_iters=case["max_iters"])
+    if sch.substituted:
+        kw["interval"] = fb.SpectralInterval(ALPHA, BETA)
+    if case.get("e0") is not None:
+        kw["e0"] = tuple(complex(*v) for v in case["e0"])
+    if case.get("sigma0_override") is not None:
+        kw["sigma0_override"] = complex(*case["sigma0_override"])
+    return fb.solve(fb.PhaseMap(chi), fb.SolverConfig(**kw))
+
+
+def _cases(group, pred=None):
+    g = load_group(group)
+    return [pytest.param(v, id=k) for k, v in g.items() if pred is None or pred(v)]
+
+
+@pytest.mark.parametrize("g", _cases("edge"))
+def test_edge_cases(g):
+    r = run_case(g["case"])
+    check(r, g)
+    if g.get("fields_file") and g["status"] == "Converged":
+        field_check(r, os.path.join(GOLDEN, g["fields_file"]))
+
+
+@pytest.mark.parametrize("g", _cases("c1"))
+def test_config1(g):
+    r = run_case(g["case"])
+    rep = check(r, g)
+    assert r.iterations == 62
+
+
+@pytest.mark.parametrize("g", _cases("c2small"))
+def test_config2_reduced(g):
+    check(run_case(g["case"]), g)
+
+
+@pytest.mark.parametrize("g", _cases("3d"))
+def test_3d(g):
+    r = run_case(g["case"])
+    check(r, g)
+    if g.get("fields_file") and g["status"] == "Converged":
+        field_check(r, os.path.join(GOLDEN, g["fields_file"]))
+
+
+@pytest.mark.parametrize("g", _cases("c5small", lambda v: int(v["case"]["name"][-3:]) % 8 == 0))
+def test_config5_sample(g):
+    check(run_case(g["case"]), g)
+
+
+def test_bit_identical_histories():
+    # reference tests/test_solvers.py:518-527: two runs, identical records
+    import paper_2001_08289_b200 as fb
+
+    pm = fb.build_square_array(32, 0.5)
+    cfg = fb.SolverConfig(scheme=fb.SchemeKind.EYRE_MILTON_SUB, sigma1=2.0,
+                          interval=fb.SpectralInterval(ALPHA, BETA), tol=1e-10)
+    r1, r2 = fb.solve(pm, cfg), fb.solve(pm, cfg)
+    assert len(r1.history) == len(r2.history)
+    for a, b in zip(r1.history, r2.history):
+        assert a.sigma_star == b.sigma_star and a.residual == b.residual
