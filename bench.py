@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 voxel-iterations/s of the FFT field iteration.
+
+Default workload = BASELINE.json configs[1] (the config the metric is quoted
+on that fits one GPU): 2048x2048 periodic cell with a centred square
+inclusion (25% phase 1), sigma2 = 1, E0 = (1, 0), stop at residual 1e-10,
+both the Eyre-Milton scheme (em) and the paper's accelerated substituted
+scheme (em_sub, (alpha, beta) = (0.25, 4.0) from the reference's
+configs/compare.cfg:14-15), sigma1 in {0.1, 10, 1000}.  One STEP = all six
+solves run to convergence.  Synthetic input (the geometry is the
+reference's own builder; no dataset exists).
+
+value   = sum over solves of N * iterations / device time of the step, with
+          the phase map already resident in HBM (CUDA events on the stream
+          the library launches on).
+e2e     = the same metric through the public API (fb.solve) with a HOST phase
+          map: host->device copy of chi and device->host copy of the history
+          inside the timed region.
+--impl reference: the CPU oracle port (oracle/fftcond_oracle.py, a bit-exact
+          numpy restatement of the reference loops) on the host cores.
+
+Multi-GPU: configs[1] does not shard (replicas only): every rank runs the
+full step on its own GPU, value = sum over ranks / max time over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_GRID = 2048
+SIDE = 0.5
+TOL = 1e-10
+MAX_ITERS = 20000
+ALPHA, BETA = 0.25, 4.0
+SOLVES = [("em", 0.1), ("em", 10.0), ("em", 1000.0), ("em_sub", 0.1), ("em_sub", 10.0), ("em_sub", 1000.0)]
+WORKLOADS = {
+    "c2": SOLVES,
+    "c2-emsub10": [("em_sub", 10.0)],
+    "c2-fast": [("em", 0.1), ("em", 10.0), ("em_sub", 0.1), ("em_sub", 10.0)],
+}
+
+
+def _peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
+
+
+def _bytes_per_voxel(scheme: str, d: int, f: float) -> dict:
+    """Algorithmic HBM bytes per voxel per launch of each sweep (2-D schedule).
+
+    V = 16 d (one complex128 d-vector); chi is 1 byte; S/T slots only move
+    on phase-1 voxels (fraction f).  See DESIGN.md section 3.
+    """
+    V = 16.0 * d
+    if scheme == "basic":
+        k = {"sweep1_rows_fwd": 2 * V + 1, "sweep2_cols_gamma": 2 * V, "sweep3_rows_inv": 3 * V + 1}
+    elif scheme == "em":
+        k = {"sweep1_rows_fwd": 3 * V + 1, "sweep2_cols_gamma": 3 * V, "sweep3_rows_inv": 2 * V + 1}
+    elif scheme == "basic_sub":
+        k = {"sweep1_rows_fwd": 2 * V + f * V + 1, "sweep2_cols_gamma": 2 * V,
+             "sweep3_rows_inv": 3 * V + 2 * f * V + 1}
+    else:
+        k = {"sweep1_rows_fwd": 3 * V + 2 * f * V + 1, "sweep2_cols_gamma": 3 * V,
+             "sweep3_rows_inv": 2 * V + 5 * f * V + 1}
+    return k
+
+
+def _survey_bytes(scheme: str, d: int, f: float) -> float:
+    """SURVEY.md 8(d) per-voxel-iteration figure for the fused 2-D schedule."""
+    V = 16.0 * d
+    return {"basic": 7 * V + 2, "em": 9 * V + 2, "basic_sub": 7 * V + 2 * f * V + 2,
+            "em_sub": 9 * V + 6 * f * V + 2}[scheme]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"fftc_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sms.append(float(parts[1]))
+                    maxs.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except OSError:
+            pass
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2] if sms else None, "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port -- test infrastructure, never the product)
+# ---------------------------------------------------------------------------
+
+def _oracle_sample(args):
+    scheme, s1, n, iters = args
+    import numpy as np
+    from oracle import fftcond_oracle as O
+
+    chi = O.centred_box(n, int(round(SIDE * n)))
+    t0 = time.perf_counter()
+    r = O.solve(chi, scheme, s1, tol=1e-300, max_iters=iters, alpha=ALPHA, beta=BETA)
+    dt = time.perf_counter() - t0
+    return n * n * r.iterations, dt
+
+
+def cpu_baseline(iters: int = 6) -> dict:
+    """Single-core oracle port on a bounded sample of the workload."""
+    tot_v, tot_t = 0, 0.0
+    for scheme, s1 in (("em", 10.0), ("em_sub", 10.0)):
+        v, t = _oracle_sample((scheme, s1, N_GRID, iters))
+        tot_v += v
+        tot_t += t
+    return {"value": tot_v / tot_t, "unit": "voxel-iterations/s", "cores": 1, "kind": "port",
+            "sample": f"em and em_sub at sigma1=10 on {N_GRID}^2, {iters} iterations each "
+                      f"(tol=1e-300 so every iteration runs), oracle/fftcond_oracle.py (numpy pocketfft, "
+                      f"bit-identical to the reference loops), {tot_t:.1f} s of CPU work"}
+
+
+def run_reference(a):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from concurrent.futures import ProcessPoolExecutor
+
+    solves = WORKLOADS[a.workload]
+    ncpu = os.cpu_count() or 1
+    procs = max(1, min(ncpu, len(solves)))
+    iters = a.ref_iters
+    jobs = [(sch, s1, N_GRID, iters) for sch, s1 in solves]
+    times, vox = [], 0
+    with ProcessPoolExecutor(max_workers=procs) as ex:
+        for step in range(a.warmup + a.steps):
+            t0 = time.perf_counter()
+            res = list(ex.map(_oracle_sample, jobs))
+            dt = time.perf_counter() - t0
+            if step >= a.warmup:
+                times.append(dt)
+                vox = sum(v for v, _ in res)
+    ms = 1e3 * sum(times) / len(times)
+    value = vox / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": "fp64 voxel-iterations/sec of the FFT iteration",
+        "value": value, "unit": "voxel-iterations/s", "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 (complex128)", "data": "synthetic (reference square-array builder)",
+        "config": _config(a),
+        "cpu_baseline": {"value": value, "unit": "voxel-iterations/s", "cores": procs, "kind": "port",
+                         "sample": f"each of the {len(solves)} solves run for {iters} iterations (bounded "
+                                   f"sample), {procs} processes on {ncpu} host CPUs; oracle/fftcond_oracle.py is "
+                                   f"the bit-exact numpy restatement of the reference loops"},
+        "e2e": {"value": value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(a):
+    solves = WORKLOADS[a.workload]
+    return {"workload": f"BASELINE configs[1]: {N_GRID}x{N_GRID} square array f=0.25, "
+                        + ", ".join(f"{s}@sigma1={v:g}" for s, v in solves) + f", tol={TOL:g}",
+            "grid": [N_GRID, N_GRID], "schemes": [s for s, _ in solves], "sigma1": [v for _, v in solves],
+            "alpha_beta": [ALPHA, BETA], "tol": TOL, "max_iters": MAX_ITERS,
+            "l2": "inputs larger than L2 (state + work fields 384-640 MB per solve >> 126 MB L2)",
+            "parallelism": "replicas" if _dist()[0] > 1 else "single GPU"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_ours(a):
+    import numpy as np
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2001_08289_b200 as fb
+    from paper_2001_08289_b200 import native
+    from paper_2001_08289_b200.solver import _solve_aug, _solve_h
+
+    solves = WORKLOADS[a.workload]
+    chi_host = np.zeros((N_GRID, N_GRID), dtype=bool)
+    m = int(round(SIDE * N_GRID))
+    lo = (N_GRID - m) // 2
+    chi_host[lo:lo + m, lo:lo + m] = True
+    frac = float(chi_host.mean())
+    cfgs = []
+    for sch, s1 in solves:
+        sk = fb.SchemeKind(sch)
+        cfgs.append(fb.SolverConfig(scheme=sk, sigma1=s1, tol=TOL, max_iters=MAX_ITERS,
+                                    interval=fb.SpectralInterval(ALPHA, BETA) if sk.substituted else None))
+    pm_dev = fb.PhaseMap(chi_host)
+    stream = torch.cuda.current_stream()
+
+    def step_device():
+        # chi resident in HBM (cached on pm_dev); fields not materialised
+        its = []
+        for cfg in cfgs:
+            if cfg.scheme.substituted:
+                r = _solve_aug(pm_dev, cfg, cfg.scheme.accelerated, want_fields=False)
+            else:
+                r = _solve_h(pm_dev, cfg, cfg.scheme.accelerated, want_fields=False)
+            its.append(r)
+        return its
+
+    def step_e2e():
+        pm = fb.PhaseMap(chi_host)  # fresh map: chi crosses host->device inside the step
+        return [fb.solve(pm, cfg) for cfg in cfgs]
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        step_device()
+    # ---- timed: device-resident ----
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    native.profile(True)
+    launches0 = native.lib().fftc_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    results = None
+    for _ in range(a.steps):
+        results = step_device()
+    e1.record(stream)
+    barrier()
+    launches = native.lib().fftc_launch_count() - launches0
+    kstats = native.kernel_stats()
+    native.profile(False)
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    ms = ms_total / a.steps
+    vox = sum(N_GRID * N_GRID * r.iterations for r in results)
+    # ---- timed: end to end through the public API, host inputs ----
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    t_wall = time.perf_counter()
+    f0.record(stream)
+    e2e_res = None
+    for _ in range(a.steps):
+        e2e_res = step_e2e()
+        _ = [r.sigma_star for r in e2e_res]
+    f1.record(stream)
+    barrier()
+    t_wall = time.perf_counter() - t_wall
+    ms_e2e = max(f0.elapsed_time(f1), 1e3 * t_wall) / a.steps
+    e2e_iters = sum(r.iterations for r in e2e_res)
+    # max over ranks
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms, ms_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+    value = ws * vox / (ms / 1e3)
+    e2e_value = ws * N_GRID * N_GRID * e2e_iters / (ms_e2e / 1e3)
+
+    # ---- roofline of the dominant kernel (from the per-launch events) ----
+    hbm, peak_src = _peaks()
+    N = N_GRID * N_GRID
+    dom = max(kstats.items(), key=lambda kv: kv[1][1]) if kstats else None
+    # algorithmic bytes: weight each scheme's per-kernel bytes by its share of launches
+    it_by_scheme = {}
+    for (sch, _), r in zip(solves, results):
+        it_by_scheme[sch] = it_by_scheme.get(sch, 0) + r.iterations
+    tot_it = sum(it_by_scheme.values())
+    roof = None
+    if dom is not None:
+        name, (nl, tms) = dom
+        bpv = sum(_bytes_per_voxel(s, 2, frac)[name] * n for s, n in it_by_scheme.items()) / tot_it
+        per_launch_ms = tms / nl
+        achieved = bpv * N / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                "bytes_per_launch": bpv * N, "avg_launch_ms": per_launch_ms, "launches": nl,
+                "share_of_step": tms / ms_total if ms_total > 0 else None}
+    survey_b = sum(_survey_bytes(s, 2, frac) * n for s, n in it_by_scheme.items()) / tot_it
+    ours_b = sum(sum(_bytes_per_voxel(s, 2, frac).values()) * n for s, n in it_by_scheme.items()) / tot_it
+    iter_roof = {"bytes_per_voxel_iter_survey": survey_b, "bytes_per_voxel_iter_schedule": ours_b,
+                 "achieved_gbs_survey_bytes": value / ws * survey_b / 1e9,
+                 "frac_survey_bytes": value / ws * survey_b / 1e9 / hbm,
+                 "achieved_gbs_schedule_bytes": value / ws * ours_b / 1e9,
+                 "frac_schedule_bytes": value / ws * ours_b / 1e9 / hbm}
+
+    line = {
+        "metric": "fp64 voxel-iterations/sec of the FFT iteration",
+        "value": value, "unit": "voxel-iterations/s", "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 (complex128)", "data": "synthetic (reference square-array builder)",
+        "config": _config(a),
+        "roofline": roof, "iteration_roofline": iter_roof,
+        "e2e": {"value": e2e_value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": N,
+                "d2h_bytes_per_step": 24 * e2e_iters + 256 * len(cfgs)},
+        "gpu_launches": int(launches), "clocks": clk,
+        "kernels": {k: {"launches": v[0], "ms_total": v[1], "ms_per_launch": v[1] / max(v[0], 1)}
+                    for k, v in kstats.items()},
+        "solves": [{"scheme": s, "sigma1": v, "iterations": r.iterations, "status": r.status.value,
+                    "sigma_star": [r.sigma_star.real, r.sigma_star.imag]} for (s, v), r in zip(solves, results)],
+    }
+    if ws == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a.cpu_iters)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--ref-iters", type=int, default=4, help="iterations per solve per reference step")
+    ap.add_argument("--cpu-iters", type=int, default=6, help="iterations per solve in cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -102,6 +102,18 @@ int fftc_solve_host(const fftc_problem* problem_with_host_chi, const fftc_params
 int fftc_fft(const fftc_problem* problem, void* data, int32_t inverse, int32_t axes_mask, void* stream);
 int fftc_gamma1(const fftc_problem* problem, const void* in, void* out, double scale, void* stream);
 
+/* Per-kernel timing.  fftc_profile(1) resets the counters and brackets every
+ * subsequent library launch with CUDA events on its stream (device time,
+ * harvested at the solver's existing synchronisation points);
+ * fftc_kernel_stats() returns up to max_entries {kind, launches, total_ms}. */
+typedef struct fftc_kstat {
+  char name[32];
+  int64_t launches;
+  double total_ms;
+} fftc_kstat;
+void fftc_profile(int32_t enable);
+int fftc_kernel_stats(fftc_kstat* out, int32_t max_entries);
+
 /* 1 if an axis of length n is supported by the compiled transforms. */
 int fftc_supported_length(int64_t n);
 

@@ -96,6 +96,16 @@ int ensure_registry() {
   fftc_fill_table_11(r.tab[11]);
   fftc_fill_table_12(r.tab[12]);
   CK(cudaDeviceGetAttribute(&r.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  {
+    // workspaces come from the stream-ordered pool; keep freed blocks cached
+    // so repeated solves do not map/unmap hundreds of MB per call
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   for (int lg = 1; lg <= MAX_LG; ++lg) {
     LTable& t = r.tab[lg];
     KInfo* all[4 + 4 + KC_COUNT + 2];
@@ -153,11 +163,74 @@ double2 hdiv(double2 a, double2 b) {
   return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
 }
 
+// ---- optional per-kernel timing (fftc_profile): event pairs per launch ----
+enum KindId { K_SWEEP1 = 0, K_MID, K_SWEEP3, K_YFWD, K_YINV, K_INIT, K_FINAL, K_OP, K_NKIND };
+const char* kKindName[K_NKIND] = {"sweep1_rows_fwd", "sweep2_cols_gamma", "sweep3_rows_inv", "y_fwd_3d",
+                                  "y_inv_3d", "init", "finalize", "operator"};
+struct KindStat {
+  long long launches = 0;
+  double ms = 0.0;
+};
+std::mutex g_prof_mu;
+bool g_profile = false;
+KindStat g_stats[K_NKIND];
+
 struct Launcher {
   cudaStream_t s;
   int num_sms;
   long long count = 0;
-  int go(const KInfo& k, long long work_lines, void** args) {
+  bool prof = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> pool;
+  Launcher(cudaStream_t st, int sms) : s(st), num_sms(sms) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    prof = g_profile;
+  }
+  ~Launcher() {
+    harvest();
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  // call only after the stream has been synchronised
+  void harvest() {
+    if (pending.empty()) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& p : pending) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
+        g_stats[p.first].launches += 1;
+        g_stats[p.first].ms += ms;
+      }
+      pool.push_back(p.second.first);
+      pool.push_back(p.second.second);
+    }
+    pending.clear();
+  }
+  int raw(const void* fn, unsigned grid, int threads, int smem, void** args, int kind) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+      e0 = ev();
+      e1 = ev();
+      cudaEventRecord(e0, s);
+    }
+    CK(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, (size_t)smem, s));
+    if (prof) {
+      cudaEventRecord(e1, s);
+      pending.push_back({kind, {e0, e1}});
+    }
+    ++count;
+    return 0;
+  }
+  int go(const KInfo& k, long long work_lines, void** args, int kind = K_OP) {
     if (!k.fn || k.max_active <= 0) {
       g_err = "kernel configuration unavailable on this device (shared memory)";
       return 1;
@@ -166,23 +239,19 @@ struct Launcher {
     long long cap = (long long)k.max_active * num_sms;
     unsigned grid = (unsigned)(need < cap ? need : cap);
     if (grid < 1) grid = 1;
-    CK(cudaLaunchKernel(k.fn, dim3(grid), dim3(k.threads), args, (size_t)k.smem, s));
-    ++count;
-    return 0;
+    return raw(k.fn, grid, k.threads, k.smem, args, kind);
   }
 };
 
 template <class F>
-int launch_elementwise(F* fn, Launcher& L, long long total, Args& a) {
+int launch_elementwise(F* fn, Launcher& L, long long total, Args& a, int kind) {
   void* args[] = {&a};
   int per = 256;
   long long need = (total + per - 1) / per;
   long long cap = (long long)L.num_sms * 8;
   unsigned grid = (unsigned)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
-  CK(cudaLaunchKernel((const void*)fn, dim3(grid), dim3(per), args, 0, L.s));
-  ++L.count;
-  return 0;
+  return L.raw((const void*)fn, grid, per, 0, args, kind);
 }
 
 }  // namespace
@@ -193,6 +262,25 @@ const char* fftc_last_error(void) { return g_err.c_str(); }
 int fftc_version(void) { return 100; }
 int64_t fftc_launch_count(void) { return g_launches.load(); }
 int fftc_supported_length(int64_t n) { return lg2_exact(n) > 0 ? 1 : 0; }
+
+void fftc_profile(int32_t enable) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_profile = enable != 0;
+  for (auto& st : g_stats) st = KindStat();
+}
+
+int fftc_kernel_stats(fftc_kstat* out, int32_t max_entries) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  int n = 0;
+  for (int k = 0; k < K_NKIND && n < max_entries; ++k) {
+    if (!g_stats[k].launches) continue;
+    snprintf(out[n].name, sizeof(out[n].name), "%s", kKindName[k]);
+    out[n].launches = g_stats[k].launches;
+    out[n].total_ms = g_stats[k].ms;
+    ++n;
+  }
+  return n;
+}
 
 int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, int64_t history_cap,
                void* E, void* J, void* aug, fftc_result* out, void* stream) {
@@ -277,7 +365,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   const size_t partial_cap = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   char* ws = nullptr;
   const size_t ws_bytes = fld * (nslots + 2) + sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring +
-                          sizeof(DevState) + 4096;
+                          sizeof(DevState) + sizeof(int2) * (size_t)ny * nz + 8192;
   CK(cudaMallocAsync((void**)&ws, ws_bytes, s));
   size_t o = 0;
   auto carve = [&](size_t bytes) {
@@ -292,6 +380,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   a.history = (double*)carve(sizeof(double) * 3 * hist_ring);
   a.hist_cap = hist_ring;
   a.st = (DevState*)carve(sizeof(DevState));
+  a.row_ext = (const int2*)carve(sizeof(int2) * (size_t)ny * nz);
   a.outE = (double2*)E;
   a.outJ = (double2*)J;
   a.outAug = (double2*)aug;
@@ -303,9 +392,9 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   cudaEvent_t ev0, ev1;
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
-  DevState* hst = nullptr;
-  CK(cudaMallocHost((void**)&hst, sizeof(DevState)));
-  Launcher Lc{s, R.num_sms};
+  thread_local DevState* hst = nullptr;
+  if (!hst) CK(cudaMallocHost((void**)&hst, sizeof(DevState)));
+  Launcher Lc(s, R.num_sms);
   const LTable& TX = R.tab[lgx];
   const LTable& TY = R.tab[lgy];
   const LTable& TZ = R.tab[d == 3 ? lgz : lgy];
@@ -315,11 +404,17 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   do {
     CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
     CK(cudaEventRecord(ev0, s));
+    {
+      const long long rows = ny * nz;
+      unsigned g = (unsigned)std::min<long long>((rows + 7) / 8, (long long)R.num_sms * 8);
+      void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
+      if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) break;
+    }
     switch (scheme) {
-      case FFTC_BASIC: rc = launch_elementwise(k_init<BASIC>, Lc, (long long)d * N, a); break;
-      case FFTC_EM: rc = launch_elementwise(k_init<EM>, Lc, (long long)d * N, a); break;
-      case FFTC_BASIC_SUB: rc = launch_elementwise(k_init<BASIC_SUB>, Lc, (long long)d * N, a); break;
-      default: rc = launch_elementwise(k_init<EM_SUB>, Lc, (long long)d * N, a); break;
+      case FFTC_BASIC: rc = launch_elementwise(k_init<BASIC>, Lc, (long long)d * N, a, K_INIT); break;
+      case FFTC_EM: rc = launch_elementwise(k_init<EM>, Lc, (long long)d * N, a, K_INIT); break;
+      case FFTC_BASIC_SUB: rc = launch_elementwise(k_init<BASIC_SUB>, Lc, (long long)d * N, a, K_INIT); break;
+      default: rc = launch_elementwise(k_init<EM_SUB>, Lc, (long long)d * N, a, K_INIT); break;
     }
     if (rc) break;
 
@@ -361,34 +456,35 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       long long todo = chunk;
       if (launched_iters + todo > pr->max_iters) todo = pr->max_iters - launched_iters;
       for (long long it = 0; it < todo && !rc; ++it) {
-        rc = Lc.go(TX.s1[scheme], row_lines, a1);
+        rc = Lc.go(TX.s1[scheme], row_lines, a1, K_SWEEP1);
         if (rc) break;
         if (d == 3) {
           // y forward of field A (and B for em-type) -- plain column pass
           Args aB = a;
           void* ayf[] = {&a, &yf};
-          rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf);
+          rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD);
           if (rc) break;
           if (em_type) {
             aB.A = a.B;
             void* ab[] = {&aB, &yfB};
-            rc = Lc.go(TY.col[KC_FWD], yf_lines, ab);
+            rc = Lc.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD);
             if (rc) break;
           }
         }
-        rc = Lc.go(*kmid, mid_lines, amid);
+        rc = Lc.go(*kmid, mid_lines, amid, K_MID);
         if (rc) break;
         if (d == 3) {
           void* ai[] = {&a, &yf};
-          rc = Lc.go(TY.col[KC_INV], yf_lines, ai);
+          rc = Lc.go(TY.col[KC_INV], yf_lines, ai, K_YINV);
           if (rc) break;
         }
-        rc = Lc.go(TX.s3[scheme], row_lines, a1);
+        rc = Lc.go(TX.s3[scheme], row_lines, a1, K_SWEEP3);
       }
       if (rc) break;
       launched_iters += todo;
       CK(cudaMemcpyAsync(hst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      Lc.harvest();
       // collect new history records from the device ring
       long long nrec = hst->nrec;
       if (nrec > history_cap) {
@@ -408,10 +504,10 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     }
     if (rc) break;
     switch (scheme) {
-      case FFTC_BASIC: rc = launch_elementwise(k_finalize<BASIC>, Lc, (long long)d * N, a); break;
-      case FFTC_EM: rc = launch_elementwise(k_finalize<EM>, Lc, (long long)d * N, a); break;
-      case FFTC_BASIC_SUB: rc = launch_elementwise(k_finalize<BASIC_SUB>, Lc, (long long)d * N, a); break;
-      default: rc = launch_elementwise(k_finalize<EM_SUB>, Lc, (long long)d * N, a); break;
+      case FFTC_BASIC: rc = launch_elementwise(k_finalize<BASIC>, Lc, (long long)d * N, a, K_FINAL); break;
+      case FFTC_EM: rc = launch_elementwise(k_finalize<EM>, Lc, (long long)d * N, a, K_FINAL); break;
+      case FFTC_BASIC_SUB: rc = launch_elementwise(k_finalize<BASIC_SUB>, Lc, (long long)d * N, a, K_FINAL); break;
+      default: rc = launch_elementwise(k_finalize<EM_SUB>, Lc, (long long)d * N, a, K_FINAL); break;
     }
     if (rc) break;
     CK(cudaEventRecord(ev1, s));
@@ -440,7 +536,6 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   out->kernel_launches = Lc.count;
   g_launches += Lc.count;
   cudaFreeAsync(ws, s);
-  cudaFreeHost(hst);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   if (!rc) {
@@ -552,7 +647,7 @@ int fftc_fft(const fftc_problem* pb, void* data, int32_t inverse, int32_t axes_m
   cudaStream_t s = (cudaStream_t)stream;
   Scratch sc;
   if (sc.alloc(a, R.num_sms, s)) return 1;
-  Launcher Lc{s, R.num_sms};
+  Launcher Lc(s, R.num_sms);
   for (int ax = 0; ax < g.d; ++ax)
     if (axes_mask & (1 << ax))
       if (int rc = run_axis(Lc, a, g, ax, inverse != 0, 1.0)) return rc;
@@ -586,7 +681,7 @@ int fftc_gamma1(const fftc_problem* pb, const void* in, void* out, double scale,
   if (in != out) CK(cudaMemcpyAsync(out, in, sizeof(double2) * g.d * g.N, cudaMemcpyDeviceToDevice, s));
   Scratch sc;
   if (sc.alloc(a, R.num_sms, s)) return 1;
-  Launcher Lc{s, R.num_sms};
+  Launcher Lc(s, R.num_sms);
   int rc = run_axis(Lc, a, g, 0, false, 1.0);
   if (!rc && g.d == 3) rc = run_axis(Lc, a, g, 1, false, 1.0);
   if (!rc) {
@@ -643,7 +738,7 @@ int fftc_debug_project(const fftc_problem* pb, void* data, void* stream) {
   a.tw[2] = g.d == 3 ? R.tw[g.lgz] : R.tw[g.lgy];
   Scratch sc;
   if (sc.alloc(a, R.num_sms, s)) return 1;
-  Launcher Lc{s, R.num_sms};
+  Launcher Lc(s, R.num_sms);
   ColGeom mid{};
   const KInfo* kmid;
   if (g.d == 2) {

@@ -205,25 +205,44 @@ __device__ __forceinline__ int pos_last(bool inv, int t, int i) {
 template <int PS>
 __device__ __forceinline__ int padpos(int p) { return p + (p >> PS); }
 
-// Build w^r, r = 0..R-1 from table loads of w^1, w^2, w^4, w^8 (w = tw[m]).
-template <int R>
-__device__ __forceinline__ void twiddle_powers(double2* w, const double2* __restrict__ tw, int m, int L) {
-  w[0] = make_double2(1.0, 0.0);
-  if constexpr (R >= 2) w[1] = __ldg(&tw[m]);
-  if constexpr (R >= 4) {
-    w[2] = __ldg(&tw[(2 * m) & (L - 1)]);
-    w[3] = cmul(w[1], w[2]);
-  }
-  if constexpr (R >= 8) {
-    w[4] = __ldg(&tw[(4 * m) & (L - 1)]);
-    w[5] = cmul(w[1], w[4]);
-    w[6] = cmul(w[2], w[4]);
-    w[7] = cmul(w[3], w[4]);
-  }
-  if constexpr (R >= 16) {
-    w[8] = __ldg(&tw[(8 * m) & (L - 1)]);
+// Multiply element r of every channel by w^r (w = tw[m], direction INV),
+// r = 1..R-1.  Powers come from table loads of w, w^2, w^4, w^8 and at most
+// three complex products; each power is applied as soon as it is formed so
+// only a handful of twiddles are live at once.
+template <int C, int E, bool INV>
+__device__ __forceinline__ void twmul(double2 (&v)[C][E], int idx, double2 w) {
 #pragma unroll
-    for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+  for (int c = 0; c < C; ++c) v[c][idx] = ctw<INV>(v[c][idx], w);
+}
+
+template <int R, int C, int E, bool INV>
+__device__ __forceinline__ void apply_twiddles(double2 (&v)[C][E], int base, const double2* __restrict__ tw, int m) {
+  const double2 w1 = __ldg(&tw[m]);
+  twmul<C, E, INV>(v, base + 1, w1);
+  if constexpr (R >= 4) {
+    const double2 w2 = __ldg(&tw[2 * m]);
+    twmul<C, E, INV>(v, base + 2, w2);
+    const double2 w3 = cmul(w1, w2);
+    twmul<C, E, INV>(v, base + 3, w3);
+    if constexpr (R >= 8) {
+      const double2 w4 = __ldg(&tw[4 * m]);
+      twmul<C, E, INV>(v, base + 4, w4);
+      twmul<C, E, INV>(v, base + 5, cmul(w1, w4));
+      twmul<C, E, INV>(v, base + 6, cmul(w2, w4));
+      const double2 w7 = cmul(w3, w4);
+      twmul<C, E, INV>(v, base + 7, w7);
+      if constexpr (R >= 16) {
+        const double2 w8 = __ldg(&tw[8 * m]);
+        twmul<C, E, INV>(v, base + 8, w8);
+        twmul<C, E, INV>(v, base + 9, cmul(w1, w8));
+        twmul<C, E, INV>(v, base + 10, cmul(w2, w8));
+        twmul<C, E, INV>(v, base + 11, cmul(w3, w8));
+        twmul<C, E, INV>(v, base + 12, cmul(w4, w8));
+        twmul<C, E, INV>(v, base + 13, cmul(cmul(w1, w4), w8));
+        twmul<C, E, INV>(v, base + 14, cmul(cmul(w2, w4), w8));
+        twmul<C, E, INV>(v, base + 15, cmul(w7, w8));
+      }
+    }
   }
 }
 
@@ -237,15 +256,7 @@ __device__ __forceinline__ void stage_compute(double2 (&v)[C][E], int t, const d
 #pragma unroll
   for (int b = 0; b < E / R; ++b) {
     const int j = t + b * T;
-    if constexpr (Ns > 1) {
-      const int k = j & (Ns - 1);
-      double2 w[R];
-      twiddle_powers<R>(w, tw, k * (L / (Ns * R)), L);
-#pragma unroll
-      for (int c = 0; c < C; ++c)
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[c][b * R + r] = ctw<INV>(v[c][b * R + r], w[r]);
-    }
+    if constexpr (Ns > 1) apply_twiddles<R, C, E, INV>(v, b * R, tw, (j & (Ns - 1)) * (L / (Ns * R)));
 #pragma unroll
     for (int c = 0; c < C; ++c) dftR<R, INV>(&v[c][b * R]);
   }

@@ -17,7 +17,10 @@ constexpr int E_ROW = L >= 8 ? 8 : L;
 constexpr int T_ROW = L / E_ROW;
 constexpr int G_ROW = T_ROW >= 64 ? 1 : 64 / T_ROW;
 // columns: radix-8, strips of 2 columns (32-B sectors); 1 column at 4096
-constexpr int E_COL = L >= 8 ? 8 : L;
+#ifndef FFTC_E_COL
+#define FFTC_E_COL 8
+#endif
+constexpr int E_COL = L >= FFTC_E_COL ? FFTC_E_COL : L;
 constexpr int T_COL = L / E_COL;
 constexpr int W2 = L >= 4096 ? 1 : 2;
 constexpr int G2 = (T_COL * W2) >= 64 ? 1 : 64 / (T_COL * W2);
@@ -36,6 +39,13 @@ template <int C, int G>
 constexpr int row_smem() {
   return G * C * Plan<L, E_ROW>::LP * (int)sizeof(double2);
 }
+
+// component-split 2-D projection sweep (needs at least 8 threads per line
+// so that a warp holds whole (t, component, column) quads)
+constexpr int E_M2 = L >= 16 ? 16 : L;
+constexpr int T_M2 = L / E_M2;
+constexpr bool USE_M2 = T_M2 >= 8 && L <= 2048;
+constexpr int m2_smem() { return 4 * (Plan<L, E_M2>::LP + 2) * (int)sizeof(double2); }
 
 template <class K>
 inline KInfo make(K* fn, int threads, int smem, int lines) {
@@ -70,8 +80,14 @@ void FFTC_CAT(fftc_fill_table_, FFTC_LG)(fftc::LTable& t) {
   t.s3[EM_SUB] = make(k_sweep3<EM_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   t.row_fwd = make(k_row_plain<false, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   t.row_inv = make(k_row_plain<true, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
-  t.col[KC_MID2_BASIC] = make(k_col<MID_BASIC, L, E_COL, W2, 2, G2>, G2 * W2 * T_COL, col_smem<2, W2, G2>(), G2);
-  t.col[KC_MID2_EM] = make(k_col<MID_EM, L, E_COL, W2, 2, G2>, G2 * W2 * T_COL, col_smem<2, W2, G2>(), G2);
+  if constexpr (USE_M2) {
+    t.col[KC_MID2_BASIC] = make(k_mid2<MID_BASIC, L, E_M2>, 4 * T_M2, m2_smem(), 1);
+    t.col[KC_MID2_EM] = make(k_mid2<MID_EM, L, E_M2>, 4 * T_M2, m2_smem(), 1);
+    t.col_w = 2;
+  } else {
+    t.col[KC_MID2_BASIC] = make(k_col<MID_BASIC, L, E_COL, W2, 2, G2>, G2 * W2 * T_COL, col_smem<2, W2, G2>(), G2);
+    t.col[KC_MID2_EM] = make(k_col<MID_EM, L, E_COL, W2, 2, G2>, G2 * W2 * T_COL, col_smem<2, W2, G2>(), G2);
+  }
   t.col[KC_MID3_BASIC] = make(k_col<MID_BASIC, L, E_COL, W3, 3, G3>, G3 * W3 * T_COL, col_smem<3, W3, G3>(), G3);
   t.col[KC_MID3_EM] = make(k_col<MID_EM, L, E_COL, W3, 3, G3>, G3 * W3 * T_COL, col_smem<3, W3, G3>(), G3);
   t.col[KC_FWD] = make(k_col<COL_FWD, L, E_COL, WP, 1, GP>, GP * WP * T_COL, col_smem<1, WP, GP>(), GP);

@@ -53,10 +53,18 @@ struct DevState {
   unsigned int pad1;
 };
 
+// Bulk L2 prefetch of a contiguous range (one instruction, no registers):
+// issued for the NEXT line while the current line's FFT runs, so its loads
+// hit L2 instead of paying the HBM round trip on the critical path.
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  if (bytes >= 16) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15u) : "memory");
+}
+
 struct Args {
   int d, nx, ny, nz;
   long long N;
   const uint8_t* chi;
+  const int2* row_ext;  // per row (z,y): [first, last+1) x-extent of phase 1 (empty: x0 >= x1)
   double2* X[3];  // state slots: e_raw | Q_raw, S_raw, T_raw
   double2* A;     // work field 0 (d*N)
   double2* B;     // work field 1 (d*N)
@@ -212,7 +220,7 @@ __device__ __forceinline__ void pinned_flux(const Args& a, bool in1, double2 jq_
 // ----------------------------------------------------------------------------
 // stopping monitor (solvers.py:243-277), one thread
 // ----------------------------------------------------------------------------
-static __device__ __noinline__ void monitor_step(const Args& a, double total_sq) {
+static __device__ __forceinline__ void monitor_step(const Args& a, double total_sq) {
   DevState* st = a.st;
   double2 jm[3];
   double den2 = 0.0;
@@ -281,6 +289,30 @@ struct SyncAll {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
 
+// L2 prefetch of everything a row sweep reads for line `ln` = (c, row).
+// S/T slots are fetched only over the row's phase-1 extent.
+template <int S, int L, bool SWEEP3>
+__device__ __forceinline__ void prefetch_row_inputs(const Args& a, long long ln, long long lines, long long rows) {
+  if (ln >= lines) return;
+  const int c = (int)(ln / rows);
+  const long long row = ln - (long long)c * rows;
+  const size_t off = (size_t)c * a.N + (size_t)row * L;
+  constexpr unsigned RB = (unsigned)(L * sizeof(double2));
+  l2_prefetch(a.chi + (size_t)row * L, L);
+  if (SWEEP3) l2_prefetch(a.A + off, RB);
+  if (!SWEEP3 || S == BASIC || S == BASIC_SUB) l2_prefetch(a.X[0] + off, RB);
+  if (S == BASIC_SUB || S == EM_SUB) {
+    const int2 ext = a.row_ext[row];
+    if (ext.x < ext.y) {
+      const int x0 = ext.x & ~1;  // 32-B aligned start
+      const unsigned nb = (unsigned)((ext.y - x0) * sizeof(double2) + 15) & ~15u;
+      if (SWEEP3 && S == EM_SUB) l2_prefetch(a.X[0] + off + x0, nb);
+      l2_prefetch(a.X[1] + off + x0, nb);
+      if (S == EM_SUB) l2_prefetch(a.X[2] + off + x0, nb);
+    }
+  }
+}
+
 // ============================================================================
 // sweep 1: rows (x-pass), forward.  Line = (component c, row r); a CTA runs
 // G lines at a time (one per thread group of T = L/E threads).
@@ -319,6 +351,7 @@ __global__ void __launch_bounds__(G*(L / E)) k_sweep1(Args a) {
     const size_t off = (size_t)c * a.N + (size_t)row * L;
     const uint8_t* chi = a.chi + (size_t)row * L;
     const double2 dl = a.st->delta[c];
+    if (t == 0) prefetch_row_inputs<S, L, false>(a, line + (long long)gridDim.x * G, lines, rows);
     double2 v[C][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
@@ -401,6 +434,7 @@ __global__ void __launch_bounds__(G*(L / E)) k_sweep3(Args a) {
     const size_t off = (size_t)c * a.N + (size_t)row * L;
     const uint8_t* chi = a.chi + (size_t)row * L;
     const double2 dl = a.st->delta[c];
+    if (t == 0) prefetch_row_inputs<S, L, true>(a, line + (long long)gridDim.x * G, lines, rows);
     double2 v[1][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) v[0][i] = live ? a.A[off + pos_first<L, E>(true, t, i)] : czero();
@@ -623,6 +657,94 @@ __global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
     if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
       monitor_step(a, tot[0] * (double)a.N + a.st->js2);
   }
+}
+
+// per-row x-extent of phase 1 (used to bound S/T prefetches); one warp per row
+static __global__ void __launch_bounds__(256) k_row_extent(const uint8_t* __restrict__ chi, int nx, long long rows,
+                                                     int2* __restrict__ ext) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < rows; r += nw) {
+    int lo = nx, hi = -1;
+    for (int x = lane; x < nx; x += 32)
+      if (chi[(size_t)r * nx + x]) {
+        lo = min(lo, x);
+        hi = max(hi, x);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) ext[r] = make_int2(lo, hi + 1);
+  }
+}
+
+// ============================================================================
+// 2-D projection sweep, component-split variant (the hot 2-D sweep 2).
+// One thread carries ONE component of one column (E = 16 per thread, radix-16
+// stages: two shared-memory exchanges per direction).  Lane layout inside a
+// warp: bit 0 = column of the 2-wide strip, bit 1 = component, bits 2..4 =
+// low bits of t; so the partner holding the other component of the same
+// (column, t) is lane ^ 2 and the Gamma projection needs one complex shuffle
+// per element (the partial dot product k_c F_c).  A warp touches 8 rows x 2
+// components x 32 B: every 32-B sector it reads or writes is fully used.
+// ============================================================================
+template <int MODE, int L, int E>
+__global__ void __launch_bounds__(4 * (L / E)) k_mid2(Args a, ColGeom gm) {
+  using P = Plan<L, E>;
+  constexpr int T = P::T;
+  constexpr int NQ = 1;
+  constexpr int SKEW = 2;                    // 4 channel buffers at bank offsets 0,2,4,6
+  extern __shared__ double2 smem[];
+  if (!a.op_mode && a.st->stopped) return;
+  const int col = threadIdx.x & 1, comp = (threadIdx.x >> 1) & 1, t = threadIdx.x >> 2;
+  double2* mybuf = smem + (comp * 2 + col) * (P::LP + SKEW);
+  const SmemBuf buf{mybuf, 0};
+  const int nfields = (MODE == MID_EM) ? 2 : 1;
+  const long long lines = (long long)gm.nstrips * nfields;
+  double acc[NQ] = {0.0};
+  for (long long line = blockIdx.x; line < lines; line += gridDim.x) {
+    const int f = (int)(line / gm.nstrips);
+    const int strip = (int)(line - (long long)f * gm.nstrips);
+    const int x = strip * 2 + col;
+    double2* F = ((f == 0) ? a.A : a.B) + (size_t)comp * a.N + x;
+    double2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[0][i] = F[(size_t)pos_first<L, E>(false, t, i) * a.nx];
+    fft_line<L, E, 1, false>(v, t, a.tw[1], buf, SyncAll{});
+    const double kx = (double)wavenum(x, a.nx);
+    const bool parseval_only = (MODE == MID_EM) && f == 1;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const double ky = (double)wavenum(pos_last<L, E>(false, t, i), a.ny);
+      const double kc = comp ? ky : kx;
+      const double k2 = kx * kx + ky * ky;
+      const double ik2 = (k2 != 0.0) ? (1.0 / k2) * a.gscale : 0.0;
+      const double2 mine = cscale(v[0][i], kc);
+      double2 other;
+      other.x = __shfl_xor_sync(0xffffffffu, mine.x, 2);
+      other.y = __shfl_xor_sync(0xffffffffu, mine.y, 2);
+      // same operand order in both lanes: kx F_x + ky F_y (spectral_ops.py:124)
+      double2 dot = comp ? cadd(other, mine) : cadd(mine, other);
+      dot = cscale(dot, ik2);
+      if (MODE == MID_BASIC || parseval_only) {
+        const double2 g = cscale(dot, kc);
+        acc[0] += cabs2(cscale(g, a.inv_n));
+        v[0][i] = g;
+      } else {
+        v[0][i] = csub(v[0][i], cscale(dot, 2.0 * kc));
+      }
+    }
+    if (parseval_only) continue;  // uniform per CTA (one line per trip)
+    fft_line<L, E, 1, true>(v, t, a.tw[1], buf, SyncAll{});
+#pragma unroll
+    for (int i = 0; i < E; ++i) F[(size_t)pos_last<L, E>(true, t, i) * a.nx] = v[0][i];
+  }
+  double tot[NQ];
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
+    monitor_step(a, tot[0] * (double)a.N + a.st->js2);
 }
 
 // ============================================================================

@@ -23,6 +23,8 @@ EXPORTS = (
     "fftc_launch_count",
     "fftc_fft",
     "fftc_gamma1",
+    "fftc_profile",
+    "fftc_kernel_stats",
 )
 
 FFTC_CONVERGED, FFTC_MAX_ITERS, FFTC_DIVERGED = 0, 1, 2
@@ -46,6 +48,10 @@ class Result(C.Structure):
                 ("sigma_star", C.c_double * 2), ("mean_E", (C.c_double * 2) * 3),
                 ("mean_J", (C.c_double * 2) * 3), ("kernel_launches", C.c_int64),
                 ("device_ms", C.c_double)]
+
+
+class KStat(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double)]
 
 
 _lock = threading.Lock()
@@ -76,6 +82,10 @@ def lib():
         L.fftc_fft.restype = C.c_int
         L.fftc_gamma1.argtypes = [C.POINTER(Problem), vp, vp, C.c_double, vp]
         L.fftc_gamma1.restype = C.c_int
+        L.fftc_profile.argtypes = [C.c_int32]
+        L.fftc_profile.restype = None
+        L.fftc_kernel_stats.argtypes = [C.POINTER(KStat), C.c_int32]
+        L.fftc_kernel_stats.restype = C.c_int
         L.fftc_supported_length.argtypes = [i64]
         L.fftc_supported_length.restype = C.c_int
         L.fftc_last_error.argtypes = []
@@ -84,6 +94,17 @@ def lib():
         L.fftc_launch_count.restype = C.c_int64
         _lib = L
         return L
+
+
+def profile(enable: bool):
+    lib().fftc_profile(1 if enable else 0)
+
+
+def kernel_stats() -> dict:
+    """{kind: (launches, total device ms)} since the last profile(True)."""
+    buf = (KStat * 16)()
+    n = lib().fftc_kernel_stats(buf, 16)
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(n)}
 
 
 def last_error() -> str:
