@@ -2,6 +2,7 @@
 // L = 2^FFTC_LG and register it.  Included by the generated inst_<lg>.cu
 // files so the ~170 kernels compile in parallel translation units.
 #include "sweeps.cuh"
+#include "rows_tma.cuh"
 #include "kernel_table.h"
 
 #ifndef FFTC_LG
@@ -12,10 +13,12 @@ namespace fftc {
 namespace inst_detail {
 
 constexpr int L = 1 << FFTC_LG;
-// rows: radix-8 lines, at least 64 threads per CTA
-constexpr int E_ROW = L >= 8 ? 8 : L;
+// rows: radix-16 lines; sweep 1 splits its channels across thread groups
+constexpr int E_ROW = L >= 16 ? 16 : L;
 constexpr int T_ROW = L / E_ROW;
-constexpr int G_ROW = T_ROW >= 64 ? 1 : 64 / T_ROW;
+constexpr int G_ROW = T_ROW >= 128 ? 1 : 128 / T_ROW;     // sweep 3 / plain: lines per CTA
+constexpr int G_ROW1 = T_ROW >= 128 ? 1 : 128 / T_ROW;    // sweep 1, one channel
+constexpr int G_ROW2 = T_ROW >= 64 ? 1 : 64 / T_ROW;      // sweep 1, two channels
 // columns: radix-8, strips of 2 columns (32-B sectors); 1 column at 4096
 #ifndef FFTC_E_COL
 #define FFTC_E_COL 8
@@ -57,6 +60,20 @@ inline KInfo make(K* fn, int threads, int smem, int lines) {
   return k;
 }
 
+template <int LL>
+inline void fill_tma(LTable& t) {
+  if constexpr (LL >= 512) {  // TMA-staged persistent row sweeps
+#define FFTC_TMA(SCH)                                                                                   \
+  t.s1[SCH] = make(k_rows_tma<SCH, 1, LL>, RowTma<SCH, 1, LL>::THREADS, RowTma<SCH, 1, LL>::SMEM, 1); \
+  t.s3[SCH] = make(k_rows_tma<SCH, 3, LL>, RowTma<SCH, 3, LL>::THREADS, RowTma<SCH, 3, LL>::SMEM, 1);
+    FFTC_TMA(BASIC)
+    FFTC_TMA(EM)
+    FFTC_TMA(BASIC_SUB)
+    FFTC_TMA(EM_SUB)
+#undef FFTC_TMA
+  }
+}
+
 }  // namespace inst_detail
 }  // namespace fftc
 
@@ -70,14 +87,15 @@ void FFTC_CAT(fftc_fill_table_, FFTC_LG)(fftc::LTable& t) {
   t.col_w = W2;
   t.col3_w = W3;
   const int trow = G_ROW * T_ROW;
-  t.s1[BASIC] = make(k_sweep1<BASIC, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
-  t.s1[EM] = make(k_sweep1<EM, L, E_ROW, G_ROW>, trow, row_smem<2, G_ROW>(), G_ROW);
-  t.s1[BASIC_SUB] = make(k_sweep1<BASIC_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
-  t.s1[EM_SUB] = make(k_sweep1<EM_SUB, L, E_ROW, G_ROW>, trow, row_smem<2, G_ROW>(), G_ROW);
+  t.s1[BASIC] = make(k_sweep1<BASIC, L, E_ROW, G_ROW1>, G_ROW1 * T_ROW, row_smem<1, G_ROW1>(), G_ROW1);
+  t.s1[EM] = make(k_sweep1<EM, L, E_ROW, G_ROW2>, 2 * G_ROW2 * T_ROW, row_smem<2, G_ROW2>(), G_ROW2);
+  t.s1[BASIC_SUB] = make(k_sweep1<BASIC_SUB, L, E_ROW, G_ROW1>, G_ROW1 * T_ROW, row_smem<1, G_ROW1>(), G_ROW1);
+  t.s1[EM_SUB] = make(k_sweep1<EM_SUB, L, E_ROW, G_ROW2>, 2 * G_ROW2 * T_ROW, row_smem<2, G_ROW2>(), G_ROW2);
   t.s3[BASIC] = make(k_sweep3<BASIC, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   t.s3[EM] = make(k_sweep3<EM, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   t.s3[BASIC_SUB] = make(k_sweep3<BASIC_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   t.s3[EM_SUB] = make(k_sweep3<EM_SUB, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
+  fill_tma<L>(t);
   t.row_fwd = make(k_row_plain<false, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   t.row_inv = make(k_row_plain<true, L, E_ROW, G_ROW>, trow, row_smem<1, G_ROW>(), G_ROW);
   if constexpr (USE_M2) {

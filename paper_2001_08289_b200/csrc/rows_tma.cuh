@@ -1,0 +1,214 @@
+// rows_tma.cuh -- TMA-staged row sweeps (sweep 1 and sweep 3) for L >= 64.
+//
+// Same algebra as k_sweep1 / k_sweep3 (reference solvers.py:300-321 and
+// :395-432), different data movement, the B200 way:
+//   * a persistent CTA walks its lines (c, row) with stride gridDim.x;
+//   * the full rows a line needs (sweep 1: the state row X0; sweep 3: the
+//     y-inverted work row A, plus X0 for basic-type schemes) and the phase
+//     row chi are fetched with cp.async.bulk (TMA bulk copy) into a ring of
+//     NSTAGE shared-memory stages completed on mbarriers, NSTAGE-1 lines
+//     ahead -- loads in flight hold no registers and no warps;
+//   * the stage's main row doubles as the FFT exchange buffer once every
+//     thread has read its inputs (padded layout, bank-conflict free);
+//   * S/T slots (phase 1 only) are read straight from global memory after an
+//     L2 bulk prefetch of the row's phase-1 extent one line ahead.
+#pragma once
+#include "sweeps.cuh"
+
+namespace fftc {
+
+template <int S, int SW, int L>
+struct RowTma {
+  static constexpr int E = 16;
+  static constexpr int T = L / E;
+  static constexpr int CH = (SW == 1) ? Sweep1Traits<S>::C : 1;
+  static constexpr int THREADS = CH * T;
+  static constexpr bool X0_ROW = (SW == 3) && (S == BASIC || S == BASIC_SUB);  // extra staged row
+  static constexpr int LP = Plan<L, E>::LP;
+  static constexpr int CHI_OFF = LP + (X0_ROW ? L : 0);      // double2 units
+  static constexpr int STAGE = CHI_OFF + L / 16;             // chi row = L bytes
+  static constexpr int NSTAGE = 2;
+  static constexpr int XBUF = (CH == 2) ? LP : 0;            // exchange buffer of channel 1
+  static constexpr int SMEM = (NSTAGE * STAGE + XBUF) * (int)sizeof(double2);
+  static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + L);
+};
+
+template <int S, int SW, int L>
+__device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, uint64_t* bar, long long line,
+                                               long long rows) {
+  using K = RowTma<S, SW, L>;
+  const int c = (int)(line / rows);
+  const long long row = line - (long long)c * rows;
+  const size_t off = (size_t)c * a.N + (size_t)row * L;
+  mbar_expect_tx(bar, K::TX);
+  bulk_g2s(stage, (SW == 1 ? a.X[0] : a.A) + off, (unsigned)(L * sizeof(double2)), bar);
+  if constexpr (K::X0_ROW) bulk_g2s(stage + K::LP, a.X[0] + off, (unsigned)(L * sizeof(double2)), bar);
+  bulk_g2s(stage + K::CHI_OFF, a.chi + (size_t)row * L, (unsigned)L, bar);
+}
+
+// L2 prefetch of the phase-1 extent of the S/T (and em_sub sweep-3 Q) rows
+template <int S, int SW, int L>
+__device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, long long line, long long lines, long long rows) {
+  if (!(S == BASIC_SUB || S == EM_SUB) || line >= lines) return;
+  const int c = (int)(line / rows);
+  const long long row = line - (long long)c * rows;
+  const int2 ext = a.row_ext[row];
+  if (ext.x >= ext.y) return;
+  const size_t off = (size_t)c * a.N + (size_t)row * L + (ext.x & ~1);
+  const unsigned nb = (unsigned)((ext.y - (ext.x & ~1)) * sizeof(double2) + 15) & ~15u;
+  if (SW == 3 && S == EM_SUB) l2_prefetch(a.X[0] + off, nb);
+  l2_prefetch(a.X[1] + off, nb);
+  if (S == EM_SUB) l2_prefetch(a.X[2] + off, nb);
+}
+
+template <int S, int SW, int L>
+__global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : 2) k_rows_tma(Args a) {
+  using K = RowTma<S, SW, L>;
+  constexpr int E = K::E, T = K::T, CH = K::CH;
+  constexpr int NQ = (SW == 1) ? Sweep1Traits<S>::NQ : 6;
+  constexpr bool INV = (SW == 3);
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ uint64_t bars[K::NSTAGE];
+  if (a.st->stopped) return;
+  const int t = threadIdx.x % T, ch = threadIdx.x / T;
+  const bool jchan = (ch == CH - 1);
+  const long long rows = (long long)a.ny * a.nz;
+  const long long lines = rows * a.d;
+  const long long nmine = blockIdx.x < lines ? (lines - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < K::NSTAGE; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < K::NSTAGE && s < nmine; ++s)
+      rows_tma_issue<S, SW, L>(a, smem + s * K::STAGE, &bars[s], blockIdx.x + (long long)s * gridDim.x, rows);
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  double2* xbuf = smem + K::NSTAGE * K::STAGE;
+  double2* OUT = (SW == 1 && CH == 2 && ch == 1) ? a.B : a.A;
+  for (long long k = 0; k < nmine; ++k) {
+    const int s = (int)(k % K::NSTAGE);
+    const unsigned parity = (unsigned)((k / K::NSTAGE) & 1);
+    const long long line = blockIdx.x + k * gridDim.x;
+    const int c = (int)(line / rows);
+    const long long row = line - (long long)c * rows;
+    const size_t off = (size_t)c * a.N + (size_t)row * L;
+    const double2 dl = a.st->delta[c];
+    double2* st = smem + s * K::STAGE;
+    const uint8_t* chi_s = reinterpret_cast<const uint8_t*>(st + K::CHI_OFF);
+    if (threadIdx.x == blockDim.x - 1) rows_tma_prefetch_slots<S, SW, L>(a, line + gridDim.x, lines, rows);
+    mbar_wait(&bars[s], parity);
+    double2 v[1][E];
+    if constexpr (SW == 1) {
+      // ---- prologue: fields to transform (solvers.py:303-311 / :398-420) ----
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int x = pos_first<L, E>(false, t, i);
+        const bool in1 = chi_s[x] != 0;
+        const double2 q = st[x];
+        if constexpr (S == BASIC) {
+          const double2 j = cmul(sigma_at(a, in1), cadd(q, dl));
+          v[0][i] = j;
+          acc_c<NQ>(acc, c, j);
+        } else if constexpr (S == EM) {
+          if (jchan) {
+            const double2 j = cmul(sigma_at(a, in1), cadd(q, dl));
+            v[0][i] = j;
+            acc_c<NQ>(acc, c, j);
+          } else {
+            v[0][i] = cmul(in1 ? a.sm1 : a.sm2, q);
+          }
+        } else {
+          const double2 sv = in1 ? a.X[1][off + x] : czero();
+          double2 tv = czero();
+          if constexpr (S == EM_SUB) tv = in1 ? a.X[2][off + x] : czero();
+          const AugFlux f = apply_A(a, in1, q, sv, tv);
+          if (jchan) {
+            double2 jq, js;
+            pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
+            v[0][i] = jq;
+            acc_c<NQ>(acc, c, jq);
+            if (in1) acc[NQ - 1] += cabs2(js);
+          } else {
+            v[0][i] = csub(f.jq, cmul(a.s0, q));
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[0][i] = st[pos_first<L, E>(true, t, i)];
+    }
+    __syncthreads();  // the main row becomes exchange scratch
+    double2* xb = (CH == 2 && ch == 1) ? xbuf : st;
+    fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
+    if constexpr (SW == 1) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) OUT[off + pos_last<L, E>(false, t, i)] = v[0][i];
+    } else {
+      // ---- epilogue: state update for iteration k+1 (solvers.py:303-308, :398-411) ----
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int x = pos_last<L, E>(true, t, i);
+        const bool in1 = chi_s[x] != 0;
+        const double2 gq = cscale(v[0][i], a.inv_n);
+        double2 qn;
+        if constexpr (S == BASIC) {
+          qn = csub(cadd(st[K::LP + x], dl), cmul(gq, a.inv_s0));
+          a.X[0][off + x] = qn;
+        } else if constexpr (S == EM) {
+          qn = cmul(cadd(a.two_s0_e0[c], gq), in1 ? a.inv_sum1 : a.inv_sum2);
+          a.X[0][off + x] = qn;
+        } else if constexpr (S == BASIC_SUB) {
+          const double2 q = st[K::LP + x];
+          qn = csub(cadd(q, dl), cmul(gq, a.inv_s0));
+          a.X[0][off + x] = qn;
+          if (in1) {
+            const double2 sv = a.X[1][off + x];
+            const AugFlux f = apply_A(a, true, q, sv, czero());
+            double2 jq, js;
+            pinned_flux(a, true, f.jq, f.js, dl, jq, js);
+            a.X[1][off + x] = csub(sv, cmul(js, a.inv_s0));
+          }
+        } else {
+          const double2 wq = cadd(a.two_s0_e0[c], gq);
+          double2 ws = czero(), wt = czero();
+          if (in1) {
+            const double2 q = a.X[0][off + x], sv = a.X[1][off + x], tv = a.X[2][off + x];
+            const AugFlux f = apply_A(a, true, q, sv, tv);
+            const double2 rs = csub(f.js, cmul(a.s0, sv));
+            ws = make_double2(-rs.x, -rs.y);
+            wt = csub(f.jt, cmul(a.s0, tv));
+          }
+          double2 sn, tn;
+          em_sub_update(a, in1, wq, ws, wt, qn, sn, tn);
+          a.X[0][off + x] = qn;
+          if (in1) {
+            a.X[1][off + x] = sn;
+            a.X[2][off + x] = tn;
+          }
+        }
+        acc_c<NQ>(acc, c, qn);
+      }
+    }
+    __syncthreads();  // stage s fully consumed (exchange, chi, X0 row)
+    if (threadIdx.x == 0 && k + K::NSTAGE < nmine) {
+      fence_proxy_async();
+      rows_tma_issue<S, SW, L>(a, st, &bars[s], line + (long long)K::NSTAGE * gridDim.x, rows);
+    }
+  }
+  double tot[NQ];
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0) {
+    if constexpr (SW == 1) {
+      for (int cc = 0; cc < a.d; ++cc)
+        a.st->jmean[cc] = make_double2(tot[2 * cc] * a.inv_n, tot[2 * cc + 1] * a.inv_n);
+      a.st->js2 = (NQ > 6) ? tot[NQ - 1] : 0.0;
+    } else {
+      for (int cc = 0; cc < a.d; ++cc)
+        a.st->delta[cc] = csub(a.e0[cc], make_double2(tot[2 * cc] * a.inv_n, tot[2 * cc + 1] * a.inv_n));
+    }
+  }
+}
+
+}  // namespace fftc

@@ -329,20 +329,25 @@ template <>
 struct Sweep1Traits<EM_SUB> { static constexpr int C = 2; static constexpr int NQ = 7; };
 
 template <int S, int L, int E, int G>
-__global__ void __launch_bounds__(G*(L / E)) k_sweep1(Args a) {
+__global__ void __launch_bounds__(G * Sweep1Traits<S>::C * (L / E), 2) k_sweep1(Args a) {
+  // The C output channels of a line (EM residual field R and flux J) are
+  // split across C thread groups that share the line's inputs (the second
+  // group's loads hit L1/L2), so each thread carries one channel.
   using P = Plan<L, E>;
-  constexpr int C = Sweep1Traits<S>::C;
+  constexpr int CH = Sweep1Traits<S>::C;
   constexpr int NQ = Sweep1Traits<S>::NQ;
   constexpr int T = P::T;
   extern __shared__ double2 smem[];
   if (a.st->stopped) return;
-  const int t = threadIdx.x % T, g = threadIdx.x / T;
+  const int t = threadIdx.x % T, ch = (threadIdx.x / T) % CH, g = threadIdx.x / (T * CH);
+  const bool jchan = (ch == CH - 1);  // the channel carrying the flux j / Jq
   const long long rows = (long long)a.ny * a.nz;
   const long long lines = rows * a.d;
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  SmemBuf buf{smem + g * C * P::LP, P::LP};
+  SmemBuf buf{smem + (g * CH + ch) * P::LP, 0};
+  double2* OUT = (CH == 2 && ch == 1) ? a.B : a.A;
   for (long long line0 = (long long)blockIdx.x * G; line0 < lines; line0 += (long long)gridDim.x * G) {
     const long long line = line0 + g;
     const bool live = line < lines;
@@ -351,54 +356,50 @@ __global__ void __launch_bounds__(G*(L / E)) k_sweep1(Args a) {
     const size_t off = (size_t)c * a.N + (size_t)row * L;
     const uint8_t* chi = a.chi + (size_t)row * L;
     const double2 dl = a.st->delta[c];
-    if (t == 0) prefetch_row_inputs<S, L, false>(a, line + (long long)gridDim.x * G, lines, rows);
-    double2 v[C][E];
+    if (t == 0 && ch == 0) prefetch_row_inputs<S, L, false>(a, line + (long long)gridDim.x * G, lines, rows);
+    double2 v[1][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int x = pos_first<L, E>(false, t, i);
       if (!live) {
-#pragma unroll
-        for (int cc = 0; cc < C; ++cc) v[cc][i] = czero();
+        v[0][i] = czero();
         continue;
       }
       const bool in1 = chi[x] != 0;
       if constexpr (S == BASIC) {
-        double2 e = cadd(a.X[0][off + x], dl);
-        double2 j = cmul(sigma_at(a, in1), e);  // j = sigma e  (solvers.py:310-311)
+        double2 j = cmul(sigma_at(a, in1), cadd(a.X[0][off + x], dl));  // j = sigma e  (solvers.py:310-311)
         v[0][i] = j;
         acc_c<NQ>(acc, c, j);
       } else if constexpr (S == EM) {
-        double2 er = a.X[0][off + x];
-        v[0][i] = cmul(in1 ? a.sm1 : a.sm2, er);           // r = (sigma - s0) e_raw  (:303)
-        double2 j = cmul(sigma_at(a, in1), cadd(er, dl));  // j = sigma (e_raw + delta)
-        v[1][i] = j;
-        acc_c<NQ>(acc, c, j);
+        const double2 er = a.X[0][off + x];
+        if (jchan) {
+          const double2 j = cmul(sigma_at(a, in1), cadd(er, dl));  // j = sigma (e_raw + delta)
+          v[0][i] = j;
+          acc_c<NQ>(acc, c, j);
+        } else {
+          v[0][i] = cmul(in1 ? a.sm1 : a.sm2, er);  // r = (sigma - s0) e_raw  (:303)
+        }
       } else {
-        double2 q = a.X[0][off + x];
-        double2 s = in1 ? a.X[1][off + x] : czero();
+        const double2 q = a.X[0][off + x];
+        const double2 s = in1 ? a.X[1][off + x] : czero();
         double2 tt = czero();
         if constexpr (S == EM_SUB) tt = in1 ? a.X[2][off + x] : czero();
-        AugFlux f = apply_A(a, in1, q, s, tt);  // (:412)
-        double2 jq, js;
-        pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
-        if constexpr (S == EM_SUB) {
-          v[0][i] = csub(f.jq, cmul(a.s0, q));  // Rq = Jq_raw - s0 Q_raw  (:398)
-          v[1][i] = jq;
-        } else {
+        const AugFlux f = apply_A(a, in1, q, s, tt);  // (:412)
+        if (jchan) {
+          double2 jq, js;
+          pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
           v[0][i] = jq;
+          acc_c<NQ>(acc, c, jq);
+          if (in1) acc[6] += cabs2(js);  // sum |Js|^2 chi  (:429)
+        } else {
+          v[0][i] = csub(f.jq, cmul(a.s0, q));  // Rq = Jq_raw - s0 Q_raw  (:398)
         }
-        acc_c<NQ>(acc, c, jq);
-        if (in1) acc[6] += cabs2(js);  // sum |Js|^2 chi  (:429)
       }
     }
-    fft_line<L, E, C, false>(v, t, a.tw[0], buf, SyncAll{});
+    fft_line<L, E, 1, false>(v, t, a.tw[0], buf, SyncAll{});
     if (live) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int x = pos_last<L, E>(false, t, i);
-        a.A[off + x] = v[0][i];
-        if constexpr (C == 2) a.B[off + x] = v[C - 1][i];
-      }
+      for (int i = 0; i < E; ++i) OUT[off + pos_last<L, E>(false, t, i)] = v[0][i];
     }
   }
   double tot[NQ];
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(G*(L / E)) k_sweep1(Args a) {
 // sweep 3: rows (x-pass), inverse + state update.  Line = (c, row).
 // ============================================================================
 template <int S, int L, int E, int G>
-__global__ void __launch_bounds__(G*(L / E)) k_sweep3(Args a) {
+__global__ void __launch_bounds__(G*(L / E), 2) k_sweep3(Args a) {
   using P = Plan<L, E>;
   constexpr int NQ = 6;
   constexpr int T = P::T;
