@@ -5,6 +5,7 @@
 // fused sweeps of sweeps.cuh; the stopping monitor runs on the device, so
 // the host only synchronises once per chunk of iterations to collect the
 // history ring and the stop flag.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -108,7 +109,7 @@ int ensure_registry() {
   }
   for (int lg = 1; lg <= MAX_LG; ++lg) {
     LTable& t = r.tab[lg];
-    KInfo* all[4 + 4 + KC_COUNT + 2];
+    KInfo* all[4 + 4 + KC_COUNT + 2];  // NOLINT
     int n = 0;
     all[n++] = &t.row_fwd;
     all[n++] = &t.row_inv;
@@ -117,6 +118,7 @@ int ensure_registry() {
     for (int c = 0; c < KC_COUNT; ++c) all[n++] = &t.col[c];
     for (int i = 0; i < n; ++i) {
       KInfo* k = all[i];
+      if (!k->fn) continue;  // variant not instantiated for this length
       if (k->smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k->smem);
         if (e != cudaSuccess) {  // too large for this device: mark unusable
@@ -140,6 +142,38 @@ int ensure_registry() {
   r.device = dev;
   r.filled = true;
   return 0;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// 3-D map over a (d, ny, nx) complex128 field seen as doubles {2nx, ny, d};
+// boxes of `rows` rows x one complex (16 B)
+bool make_field_map(CUtensorMap* tm, void* base, long long nx, long long ny, int d, int rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * nx), (cuuint64_t)ny, (cuuint64_t)d};
+  cuuint64_t strides[2] = {(cuuint64_t)(nx * 16), (cuuint64_t)(nx * ny * 16)};
+  cuuint32_t box[3] = {2, (cuuint32_t)rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 double2 C2(const double* p) { return make_double2(p[0], p[1]); }
@@ -421,6 +455,8 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     // column geometries
     ColGeom mid{};
     ColGeom yf{};
+    CUtensorMap tmA, tmB;
+    bool use_tma_mid = false;
     const bool em_type = (scheme == FFTC_EM || scheme == FFTC_EM_SUB);
     const KInfo* kmid;
     if (d == 2) {
@@ -430,6 +466,13 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       mid.ostride = 0;
       mid.nstrips = (int)(nx / TY.col_w);
       kmid = &TY.col[em_type ? KC_MID2_EM : KC_MID2_BASIC];
+      const KInfo& kt = TY.col[em_type ? KC_MID2T_EM : KC_MID2T_BASIC];
+      if (kt.fn && kt.max_active > 0 && !getenv("FFTC_NO_TMA_COLS") &&
+          make_field_map(&tmA, a.A, nx, ny, d, ny < 256 ? (int)ny : 256) &&
+          make_field_map(&tmB, a.B, nx, ny, d, ny < 256 ? (int)ny : 256)) {
+        kmid = &kt;
+        use_tma_mid = true;
+      }
     } else {
       mid.axis = 2;
       mid.nouter = (int)ny;
@@ -443,11 +486,14 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       yf.ostride = nx * ny;
       yf.nstrips = (int)(nx / 2);
     }
-    const long long mid_lines = (long long)mid.nouter * mid.nstrips * (em_type ? 2 : 1);
+    const long long mid_lines = use_tma_mid ? nx * (em_type ? 2 : 1)
+                                            : (long long)mid.nouter * mid.nstrips * (em_type ? 2 : 1);
     const long long row_lines = (long long)d * ny * nz;
     const long long yf_lines = (long long)yf.nouter * yf.nstrips * d;
     void* a1[] = {&a};
-    void* amid[] = {&a, &mid};
+    void* amid_std[] = {&a, &mid};
+    void* amid_tma[] = {&a, &tmA, &tmB};
+    void** amid = use_tma_mid ? amid_tma : amid_std;
     ColGeom yfB = yf;  // forward y pass of field B (em-type) uses the same geometry
 
     long long chunk = 2;

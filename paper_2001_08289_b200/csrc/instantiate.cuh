@@ -3,6 +3,7 @@
 // files so the ~170 kernels compile in parallel translation units.
 #include "sweeps.cuh"
 #include "rows_tma.cuh"
+#include "cols_tma.cuh"
 #include "kernel_table.h"
 
 #ifndef FFTC_LG
@@ -62,6 +63,10 @@ inline KInfo make(K* fn, int threads, int smem, int lines) {
 
 template <int LL>
 inline void fill_tma(LTable& t) {
+  if constexpr (LL >= 256 && LL <= 2048) {  // TMA tensor-map 2-D projection sweep
+    t.col[KC_MID2T_BASIC] = make(k_mid2_tma<MID_BASIC, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
+    t.col[KC_MID2T_EM] = make(k_mid2_tma<MID_EM, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
+  }
   if constexpr (LL >= 512) {  // TMA-staged persistent row sweeps
 #define FFTC_TMA(SCH)                                                                                   \
   t.s1[SCH] = make(k_rows_tma<SCH, 1, LL>, RowTma<SCH, 1, LL>::THREADS, RowTma<SCH, 1, LL>::SMEM, 1); \

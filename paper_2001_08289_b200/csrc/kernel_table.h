@@ -14,7 +14,8 @@ struct KInfo {
 };
 
 // column kernel variants
-enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_FWD = 4, KC_INV = 5, KC_COUNT = 6 };
+enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_FWD = 4, KC_INV = 5,
+       KC_MID2T_BASIC = 6, KC_MID2T_EM = 7, KC_COUNT = 8 };  // *T: TMA tensor-map variants (signature Args, map A, map B)
 
 struct LTable {
   int L = 0;
