@@ -398,7 +398,8 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   const int hist_ring = 1024;
   const size_t partial_cap = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   char* ws = nullptr;
-  const size_t ws_bytes = fld * (nslots + 2) + sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring +
+  const bool two_work = (scheme == FFTC_EM || scheme == FFTC_EM_SUB);  // B holds the flux transform
+  const size_t ws_bytes = fld * (nslots + (two_work ? 2 : 1)) + sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring +
                           sizeof(DevState) + sizeof(int2) * (size_t)ny * nz + 8192;
   CK(cudaMallocAsync((void**)&ws, ws_bytes, s));
   size_t o = 0;
@@ -409,7 +410,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   };
   for (int i = 0; i < nslots; ++i) a.X[i] = (double2*)carve(fld);
   a.A = (double2*)carve(fld);
-  a.B = (double2*)carve(fld);
+  a.B = two_work ? (double2*)carve(fld) : a.A;
   a.partials = (double*)carve(sizeof(double) * partial_cap);
   a.history = (double*)carve(sizeof(double) * 3 * hist_ring);
   a.hist_cap = hist_ring;

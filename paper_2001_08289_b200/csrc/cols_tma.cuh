@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
       const double ky = (double)wavenum(pos_last<L, E>(false, t, i), a.ny);
       const double kc = comp ? ky : kx;
       const double k2 = kx * kx + ky * ky;
-      const double ik2 = (k2 != 0.0) ? (1.0 / k2) * a.gscale : 0.0;
+      const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
       const double2 mine = cscale(v[0][i], kc);
       double2 other;
       other.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);

@@ -272,23 +272,50 @@ __device__ __forceinline__ void stage_exchange(double2 (&v)[C][E], int t, Buf bu
   constexpr int Ns = P::ns(INV, S);
   constexpr int R2 = P::radix(INV, S + 1);
   constexpr int T = P::T;
+  constexpr int PAD = 1 << P::PS;
+  // When the stride between a butterfly's outputs (Ns) is a multiple of the
+  // pad period, or the first stage writes a full pad period per butterfly,
+  // every padded address is the butterfly base plus a compile-time offset.
+  constexpr bool ST_CONST = (Ns % PAD == 0) || (Ns == 1 && R == PAD);
+  constexpr int LD_STRIDE = L / R2;
+  constexpr bool LD_CONST = (LD_STRIDE % PAD == 0);
 #pragma unroll
   for (int b = 0; b < E / R; ++b) {
     const int j = t + b * T;
     const int base = (j / Ns) * Ns * R + (j & (Ns - 1));
+    if constexpr (ST_CONST) {
+      const int pb = padpos<P::PS>(base);
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+      for (int r = 0; r < R; ++r) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int off = (Ns == 1) ? r : r * Ns + ((r * Ns) >> P::PS);
 #pragma unroll
-      for (int c = 0; c < C; ++c) buf(c)[padpos<P::PS>(base + r * Ns)] = v[c][b * R + r];
+        for (int c = 0; c < C; ++c) buf(c)[pb + off] = v[c][b * R + r];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) buf(c)[padpos<P::PS>(base + r * Ns)] = v[c][b * R + r];
+    }
   }
   bar();
 #pragma unroll
   for (int b = 0; b < E / R2; ++b) {
     const int j = t + b * T;
+    if constexpr (LD_CONST) {
+      const int pj = padpos<P::PS>(j);
 #pragma unroll
-    for (int r = 0; r < R2; ++r)
+      for (int r = 0; r < R2; ++r)
 #pragma unroll
-      for (int c = 0; c < C; ++c) v[c][b * R2 + r] = buf(c)[padpos<P::PS>(j + r * (L / R2))];
+        for (int c = 0; c < C; ++c) v[c][b * R2 + r] = buf(c)[pj + r * LD_STRIDE + ((r * LD_STRIDE) >> P::PS)];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R2; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c][b * R2 + r] = buf(c)[padpos<P::PS>(j + r * LD_STRIDE)];
+    }
   }
   bar();
 }
@@ -338,6 +365,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// 1/k2 for an integer-valued k2 >= 1 (|k|^2 of a wave vector): float seed
+// plus two Newton steps in fp64, branch free (the IEEE division of the
+// plain form carries a slow path per element); within 1 ulp of 1.0/k2.
+__device__ __forceinline__ double inv_k2(double k2) {
+  double y = (double)__frcp_rn((float)k2);
+  y = fma(y, fma(-k2, y, 1.0), y);
+  y = fma(y, fma(-k2, y, 1.0), y);
+  return y;
 }
 
 // signed integer wave number of index i on an n-point periodic grid

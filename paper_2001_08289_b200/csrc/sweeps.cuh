@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
           double k2 = k[0] * k[0];
 #pragma unroll
           for (int c = 1; c < C; ++c) k2 += k[c] * k[c];
-          const double ik2 = (k2 != 0.0) ? (1.0 / k2) * a.gscale : 0.0;
+          const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
           double2 dot = cscale(v[0][i], k[0]);
 #pragma unroll
           for (int c = 1; c < C; ++c) dot = cadd(dot, cscale(v[c][i], k[c]));
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(4 * (L / E)) k_mid2(Args a, ColGeom gm) {
       const double ky = (double)wavenum(pos_last<L, E>(false, t, i), a.ny);
       const double kc = comp ? ky : kx;
       const double k2 = kx * kx + ky * ky;
-      const double ik2 = (k2 != 0.0) ? (1.0 / k2) * a.gscale : 0.0;
+      const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
       const double2 mine = cscale(v[0][i], kc);
       double2 other;
       other.x = __shfl_xor_sync(0xffffffffu, mine.x, 2);
