@@ -46,6 +46,7 @@ WORKLOADS = {
     "c2": SOLVES,
     "c2-emsub10": [("em_sub", 10.0)],
     "c2-fast": [("em", 0.1), ("em", 10.0), ("em_sub", 0.1), ("em_sub", 10.0)],
+    "c5": None,  # BASELINE configs[4]: 256-point complex sigma1 sweep, em_sub, 1024^2 (see run_c5)
 }
 
 
@@ -379,6 +380,80 @@ def run_ours(a):
     return 0
 
 
+def run_c5(a):
+    """BASELINE configs[4]: 256 complex sigma1 points on the 1024^2 square array,
+    em_sub, tol 1e-8, max_iters 1000 (reference defaults), points sharded
+    round robin over the ranks ("batched over sweep points across GPUs"):
+    strong scaling, total work fixed.  Step = the whole sweep."""
+    import numpy as np
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2001_08289_b200 as fb
+    from paper_2001_08289_b200 import native
+    from paper_2001_08289_b200.sweep import _solve_local_gpu, c5_points, shard, solve_sweep
+
+    n = 1024
+    pm = fb.build_square_array(n, 0.5)
+    pts = c5_points(a.c5_points)
+    cfgs = [fb.SolverConfig(scheme=fb.SchemeKind.EYRE_MILTON_SUB, sigma1=s, tol=1e-8, max_iters=1000,
+                            interval=fb.SpectralInterval(ALPHA, BETA)) for s in pts]
+    mine = [cfgs[i] for i in shard(len(cfgs), rank, ws)]
+    _solve_local_gpu(pm, mine[:2])  # warm up
+    stream = torch.cuda.current_stream()
+    times, recs = [], None
+    launches0 = native.lib().fftc_launch_count()
+    for step in range(max(1, a.steps)):
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        recs = solve_sweep(pm, cfgs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    launches = native.lib().fftc_launch_count() - launches0
+    ms = sum(times) / len(times)
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    vox = sum(n * n * r["iterations"] for r in recs)
+    value = vox / (ms / 1e3)
+    hbm, src = _peaks()
+    V = 32.0
+    bpv = 8 * V + 7 * 0.25 * V + 2
+    conv = sum(1 for r in recs if r["status"].value == "Converged")
+    line = {"metric": "fp64 voxel-iterations/sec of the FFT iteration", "value": value,
+            "unit": "voxel-iterations/s", "n_gpus": ws, "steps": len(times), "warmup": 1, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128)",
+            "data": "synthetic (seeded sigma1 points, reference square-array builder)",
+            "config": {"workload": f"BASELINE configs[4]: {len(cfgs)} complex sigma1 points, em_sub, {n}^2, tol 1e-8, "
+                                   "max_iters 1000", "parallelism": f"points sharded over {ws} GPU(s)"},
+            "iteration_roofline": {"bytes_per_voxel_iter_schedule": bpv, "frac_schedule_bytes": value * bpv / 1e9 / hbm / ws,
+                                   "peak_gbs": hbm, "peak_source": src},
+            "gpu_launches": int(launches * ws), "points_converged": conv, "points_total": len(recs),
+            "total_iterations": sum(r["iterations"] for r in recs)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -389,7 +464,10 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=4, help="iterations per solve per reference step")
     ap.add_argument("--cpu-iters", type=int, default=6, help="iterations per solve in cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c5-points", type=int, default=256)
     a = ap.parse_args()
+    if a.workload == "c5" and a.impl == "ours":
+        return run_c5(a)
     if a.impl == "reference":
         return run_reference(a)
     return run_ours(a)

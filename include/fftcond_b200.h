@@ -81,6 +81,14 @@ typedef struct fftc_result {
 int fftc_solve(const fftc_problem* problem, const fftc_params* params, double* history,
                int64_t history_cap, void* E, void* J, void* aug, fftc_result* out, void* stream);
 
+/* BASELINE config 5: n_points independent solves on one grid (e.g. a sweep
+ * of sigma1), histories laid out [n_points][history_cap][3], one result per
+ * point.  Fields are not returned (only the per-point averages).  Replaces
+ * sequential calls of solve() such as cli.cmd_compare (cli.py:352-408) and
+ * analysis.misestimation_report (analysis.py:166-201). */
+int fftc_solve_batch(const fftc_problem* problem, const fftc_params* params, int32_t n_points,
+                     double* histories, int64_t history_cap, fftc_result* out, void* stream);
+
 /* Same contract, host-resident chi and outputs (the library copies in and
  * out; E/J/aug host buffers are nullable).  For FFI users without a device
  * allocator. */

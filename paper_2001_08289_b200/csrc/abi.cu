@@ -808,6 +808,27 @@ int fftc_debug_project(const fftc_problem* pb, void* data, void* stream) {
   return 0;
 }
 
+// Batched sweep (BASELINE config 5): n_points independent solves on one
+// grid, run back to back on one stream (the workspace comes from the warm
+// stream-ordered pool, so per-point setup is a few microseconds).
+int fftc_solve_batch(const fftc_problem* pb, const fftc_params* params, int32_t n_points, double* histories,
+                     int64_t history_cap, fftc_result* out, void* stream) {
+  g_err.clear();
+  if (!params || !out || n_points < 0) {
+    g_err = "null argument";
+    return 2;
+  }
+  for (int32_t i = 0; i < n_points; ++i) {
+    int rc = fftc_solve(pb, &params[i], histories + (size_t)i * history_cap * 3, history_cap, nullptr, nullptr,
+                        nullptr, &out[i], stream);
+    if (rc) {
+      g_err = "point " + std::to_string(i) + ": " + g_err;
+      return rc;
+    }
+  }
+  return 0;
+}
+
 int fftc_solve_host(const fftc_problem* pb, const fftc_params* pr, double* history, int64_t history_cap,
                     void* E_host, void* J_host, void* aug_host, fftc_result* out) {
   g_err.clear();

@@ -25,6 +25,7 @@ EXPORTS = (
     "fftc_gamma1",
     "fftc_profile",
     "fftc_kernel_stats",
+    "fftc_solve_batch",
 )
 
 FFTC_CONVERGED, FFTC_MAX_ITERS, FFTC_DIVERGED = 0, 1, 2
@@ -78,6 +79,9 @@ def lib():
         L.fftc_solve_host.argtypes = [C.POINTER(Problem), C.POINTER(Params), vp, i64, vp, vp, vp,
                                       C.POINTER(Result)]
         L.fftc_solve_host.restype = C.c_int
+        L.fftc_solve_batch.argtypes = [C.POINTER(Problem), C.POINTER(Params), C.c_int32, vp, i64,
+                                       C.POINTER(Result), vp]
+        L.fftc_solve_batch.restype = C.c_int
         L.fftc_fft.argtypes = [C.POINTER(Problem), vp, C.c_int32, C.c_int32, vp]
         L.fftc_fft.restype = C.c_int
         L.fftc_gamma1.argtypes = [C.POINTER(Problem), vp, vp, C.c_double, vp]

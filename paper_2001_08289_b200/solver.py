@@ -212,27 +212,44 @@ def _device_chi(pmap: PhaseMap, torch):
     return t
 
 
-def _run_device(pmap: PhaseMap, cfg: SolverConfig, scheme: SchemeKind, sigma0: complex,
-                t: complex = 1.0, p=(0j, 0j, 0j), want_fields: bool = True) -> SolveResult:
-    torch = _torch()
+def _check_grid(pmap: PhaseMap):
     L = native.lib()
-    d = pmap.dim
     for n in pmap.grid:
         if not L.fftc_supported_length(int(n)):
             raise ContractError(
                 f"grid axis of length {n} is not supported by the B200 transforms "
                 "(power-of-two lengths 2..4096)")
-    e0 = cfg.e0_vector(d)
-    chi = _device_chi(pmap, torch)
-    grid = pmap.grid
+
+
+def _problem(pmap: PhaseMap, chi) -> native.Problem:
     prob = native.Problem()
-    prob.d = d
+    prob.d = pmap.dim
     prob.n[0], prob.n[1], prob.n[2] = pmap.nx, pmap.ny, pmap.nz
     prob.chi = chi.data_ptr()
+    return prob
+
+
+def _params(cfg: SolverConfig, d: int) -> native.Params:
+    """Host-side scalar setup of one solve (reference expressions), packed for the ABI.
+
+    Raises exactly what the reference raises before its loop starts:
+    _reference_h / _reference_aug (solvers.py:221-240, :334-352), map_t and
+    solve_p (transform.py:99-168).
+    """
+    scheme = cfg.scheme
+    t, p = 1.0 + 0j, (0j, 0j, 0j)
+    if scheme.substituted:
+        t = map_t(complex(cfg.sigma1), cfg.interval)
+        sp = solve_p(cfg.interval)
+        p = (sp.p1, sp.p2, sp.p3)
+        s0 = _reference_aug(cfg, t, scheme.accelerated)
+    else:
+        s0 = _reference_h(cfg, scheme.accelerated)
+    e0 = cfg.e0_vector(d)
     par = native.Params()
     par.scheme = scheme.abi_code
     par.sigma1[:] = native.cpair(cfg.sigma1)
-    par.sigma0[:] = native.cpair(sigma0)
+    par.sigma0[:] = native.cpair(s0)
     par.t[:] = native.cpair(t)
     par.p1[:] = native.cpair(p[0])
     par.p2[:] = native.cpair(p[1])
@@ -242,12 +259,45 @@ def _run_device(pmap: PhaseMap, cfg: SolverConfig, scheme: SchemeKind, sigma0: c
     par.tol = float(cfg.tol)
     par.max_iters = int(cfg.max_iters)
     par.gamma1_scale = float(_fields._gamma1_scale)
+    return par
+
+
+def _result_from(res: native.Result, hist: np.ndarray, d: int, E=None, J=None, aug=None) -> SolveResult:
+    n = int(res.iterations)
+    aug_field = None
+    if aug is not None:
+        aug_field = AugmentedField(VectorField.from_device(aug[0]), VectorField.from_device(aug[1]),
+                                   VectorField.from_device(aug[2]))
+    return SolveResult(
+        sigma_star=complex(res.sigma_star[0], res.sigma_star[1]),
+        E_field=VectorField.from_device(E) if E is not None else None,
+        J_field=VectorField.from_device(J) if J is not None else None,
+        history=ConvergenceHistory.from_array(hist[:n]),
+        status=_STATUS[int(res.status)],
+        degenerate_flux=bool(res.degenerate_flux),
+        aug_field=aug_field,
+        mean_E=np.array([complex(res.mean_E[c][0], res.mean_E[c][1]) for c in range(d)]),
+        mean_J=np.array([complex(res.mean_J[c][0], res.mean_J[c][1]) for c in range(d)]),
+        device_ms=float(res.device_ms),
+        kernel_launches=int(res.kernel_launches),
+    )
+
+
+def _run_device(pmap: PhaseMap, cfg: SolverConfig, want_fields: bool = True) -> SolveResult:
+    par = _params(cfg, pmap.dim)  # host validation first: raises before any device work
+    torch = _torch()
+    L = native.lib()
+    _check_grid(pmap)
+    d = pmap.dim
+    chi = _device_chi(pmap, torch)
+    grid = pmap.grid
+    prob = _problem(pmap, chi)
     hist = np.empty((int(cfg.max_iters), 3), dtype=np.float64)
     E = J = aug = None
     if want_fields:
         E = torch.empty((d,) + grid, dtype=torch.complex128, device="cuda")
         J = torch.empty((d,) + grid, dtype=torch.complex128, device="cuda")
-        if scheme.substituted:
+        if cfg.scheme.substituted:
             aug = torch.empty((3, d) + grid, dtype=torch.complex128, device="cuda")
     res = native.Result()
     stream = torch.cuda.current_stream().cuda_stream
@@ -256,44 +306,25 @@ def _run_device(pmap: PhaseMap, cfg: SolverConfig, scheme: SchemeKind, sigma0: c
                       None if aug is None else aug.data_ptr(), C.byref(res), stream)
     if rc != 0:
         raise BackendError(f"fftc_solve failed ({rc}): {native.last_error()}")
-    n = int(res.iterations)
-    history = ConvergenceHistory.from_array(hist[:n])
-    sstar = complex(res.sigma_star[0], res.sigma_star[1])
-    mean_E = np.array([complex(res.mean_E[c][0], res.mean_E[c][1]) for c in range(d)])
-    mean_J = np.array([complex(res.mean_J[c][0], res.mean_J[c][1]) for c in range(d)])
-    aug_field = None
-    if aug is not None:
-        aug_field = AugmentedField(VectorField.from_device(aug[0]), VectorField.from_device(aug[1]),
-                                   VectorField.from_device(aug[2]))
-    return SolveResult(
-        sigma_star=sstar,
-        E_field=VectorField.from_device(E) if E is not None else None,
-        J_field=VectorField.from_device(J) if J is not None else None,
-        history=history,
-        status=_STATUS[int(res.status)],
-        degenerate_flux=bool(res.degenerate_flux),
-        aug_field=aug_field,
-        mean_E=mean_E,
-        mean_J=mean_J,
-        device_ms=float(res.device_ms),
-        kernel_launches=int(res.kernel_launches),
-    )
+    return _result_from(res, hist, d, E, J, aug)
 
 
 def _solve_h(pmap: PhaseMap, cfg: SolverConfig, accelerated: bool, want_fields: bool = True) -> SolveResult:
     """H-space loop (basic / em) on the device; replaces solvers.py:280-331."""
-    s0 = _reference_h(cfg, accelerated)
-    scheme = SchemeKind.EYRE_MILTON if accelerated else SchemeKind.BASIC
-    return _run_device(pmap, cfg, scheme, s0, want_fields=want_fields)
+    expected = SchemeKind.EYRE_MILTON if accelerated else SchemeKind.BASIC
+    if cfg.scheme is not expected:
+        cfg = SolverConfig(scheme=expected, sigma1=cfg.sigma1, e0=cfg.e0, tol=cfg.tol,
+                           max_iters=cfg.max_iters, sigma0_override=cfg.sigma0_override)
+    return _run_device(pmap, cfg, want_fields)
 
 
 def _solve_aug(pmap: PhaseMap, cfg: SolverConfig, accelerated: bool, want_fields: bool = True) -> SolveResult:
     """Augmented loop (basic_sub / em_sub) on the device; replaces solvers.py:366-443."""
-    t = map_t(complex(cfg.sigma1), cfg.interval)
-    params = solve_p(cfg.interval)
-    s0 = _reference_aug(cfg, t, accelerated)
-    scheme = SchemeKind.EYRE_MILTON_SUB if accelerated else SchemeKind.BASIC_SUB
-    return _run_device(pmap, cfg, scheme, s0, t, (params.p1, params.p2, params.p3), want_fields)
+    expected = SchemeKind.EYRE_MILTON_SUB if accelerated else SchemeKind.BASIC_SUB
+    if cfg.scheme is not expected:
+        cfg = SolverConfig(scheme=expected, sigma1=cfg.sigma1, interval=cfg.interval, e0=cfg.e0,
+                           tol=cfg.tol, max_iters=cfg.max_iters, sigma0_override=cfg.sigma0_override)
+    return _run_device(pmap, cfg, want_fields)
 
 
 def _check_scheme(cfg: SolverConfig, expected: SchemeKind):
