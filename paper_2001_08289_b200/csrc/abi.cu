@@ -162,18 +162,20 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// 3-D map over a (d, ny, nx) complex128 field seen as doubles {2nx, ny, d};
-// boxes of `rows` rows x one complex (16 B)
+// 4-D map over a (d, ny, nx) complex128 field seen as doubles
+// {2nx, rows, ny/rows, d}: a box {2, rows, ny/rows, 2} is one whole column
+// (both components, all ny rows, 16 B per row) in a single TMA operation.
 bool make_field_map(CUtensorMap* tm, void* base, long long nx, long long ny, int d, int rows) {
   EncodeTiledFn enc = encode_tiled();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)(2 * nx), (cuuint64_t)ny, (cuuint64_t)d};
-  cuuint64_t strides[2] = {(cuuint64_t)(nx * 16), (cuuint64_t)(nx * ny * 16)};
-  cuuint32_t box[3] = {2, (cuuint32_t)rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
+  if (!enc || ny % rows) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)(2 * nx), (cuuint64_t)rows, (cuuint64_t)(ny / rows), (cuuint64_t)d};
+  cuuint64_t strides[3] = {(cuuint64_t)(nx * 16), (cuuint64_t)(nx * 16 * rows), (cuuint64_t)(nx * ny * 16)};
+  cuuint32_t box[4] = {2, (cuuint32_t)rows, (cuuint32_t)(ny / rows), 2};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("FFTC_VERBOSE")) fprintf(stderr, "[fftc] cuTensorMapEncodeTiled failed: %d\n", (int)r);
+  return r == CUDA_SUCCESS;
 }
 
 double2 C2(const double* p) { return make_double2(p[0], p[1]); }
@@ -208,6 +210,11 @@ struct KindStat {
 std::mutex g_prof_mu;
 bool g_profile = false;
 KindStat g_stats[K_NKIND];
+
+bool debug_sync() {
+  static const bool on = getenv("FFTC_DEBUG_SYNC") != nullptr;
+  return on;
+}
 
 struct Launcher {
   cudaStream_t s;
@@ -257,6 +264,14 @@ struct Launcher {
       cudaEventRecord(e0, s);
     }
     CK(cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, (size_t)smem, s));
+    if (debug_sync()) {  // FFTC_DEBUG_SYNC=1: locate a faulting kernel
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        g_err = std::string("kernel kind ") + kKindName[kind] + " grid " + std::to_string(grid) + " block " +
+                std::to_string(threads) + " smem " + std::to_string(smem) + ": " + cudaGetErrorString(e);
+        return 1;
+      }
+    }
     if (prof) {
       cudaEventRecord(e1, s);
       pending.push_back({kind, {e0, e1}});
@@ -286,6 +301,19 @@ int launch_elementwise(F* fn, Launcher& L, long long total, Args& a, int kind) {
   unsigned grid = (unsigned)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
   return L.raw((const void*)fn, grid, per, 0, args, kind);
+}
+
+// Body-graph tail of the device-side WHILE loop: keep iterating until the
+// monitor (solvers.py:243-277, run by the last CTA of the projection sweep)
+// raises the stop flag.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const DevState* st) {
+  cudaGraphSetConditional(h, st->stopped ? 0u : 1u);
+}
+
+cudaStream_t capture_stream() {
+  thread_local cudaStream_t cs = nullptr;
+  if (!cs) cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  return cs;
 }
 
 }  // namespace
@@ -395,7 +423,13 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   // ---- workspace ----
   const int nslots = scheme == FFTC_EM_SUB ? 3 : (scheme == FFTC_BASIC_SUB ? 2 : 1);
   const size_t fld = sizeof(double2) * (size_t)d * N;
-  const int hist_ring = 1024;
+  bool use_graph;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    use_graph = !g_profile && pr->max_iters <= (1 << 20) && !getenv("FFTC_NO_GRAPH");
+  }
+  // graph mode runs the whole loop in one launch: the device keeps every record
+  const int hist_ring = use_graph ? (int)std::max<int64_t>(pr->max_iters, 16) : 1024;
   const size_t partial_cap = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   char* ws = nullptr;
   const bool two_work = (scheme == FFTC_EM || scheme == FFTC_EM_SUB);  // B holds the flux transform
@@ -416,6 +450,8 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   a.hist_cap = hist_ring;
   a.st = (DevState*)carve(sizeof(DevState));
   a.row_ext = (const int2*)carve(sizeof(int2) * (size_t)ny * nz);
+  a.dbg = getenv("FFTC_PHASE") ? (unsigned long long*)carve(sizeof(unsigned long long) * 8) : nullptr;
+  if (a.dbg) CK(cudaMemsetAsync(a.dbg, 0, sizeof(unsigned long long) * 8, s));
   a.outE = (double2*)E;
   a.outJ = (double2*)J;
   a.outAug = (double2*)aug;
@@ -497,57 +533,116 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     void** amid = use_tma_mid ? amid_tma : amid_std;
     ColGeom yfB = yf;  // forward y pass of field B (em-type) uses the same geometry
 
-    long long chunk = 2;
-    long long launched_iters = 0;
-    while (!stopped) {
-      long long todo = chunk;
-      if (launched_iters + todo > pr->max_iters) todo = pr->max_iters - launched_iters;
-      for (long long it = 0; it < todo && !rc; ++it) {
-        rc = Lc.go(TX.s1[scheme], row_lines, a1, K_SWEEP1);
-        if (rc) break;
-        if (d == 3) {
-          // y forward of field A (and B for em-type) -- plain column pass
-          Args aB = a;
-          void* ayf[] = {&a, &yf};
-          rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD);
-          if (rc) break;
-          if (em_type) {
-            aB.A = a.B;
-            void* ab[] = {&aB, &yfB};
-            rc = Lc.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD);
-            if (rc) break;
-          }
+    // one reference iteration (solvers.py:300-321 / :395-432) = these launches
+    auto launch_iter = [&](Launcher& L) -> int {
+      int r = L.go(TX.s1[scheme], row_lines, a1, K_SWEEP1);
+      if (r) return r;
+      if (d == 3) {
+        // y forward of field A (and B for em-type) -- plain column pass
+        Args aB = a;
+        void* ayf[] = {&a, &yf};
+        if ((r = L.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD))) return r;
+        if (em_type) {
+          aB.A = a.B;
+          void* ab[] = {&aB, &yfB};
+          if ((r = L.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD))) return r;
         }
-        rc = Lc.go(*kmid, mid_lines, amid, K_MID);
-        if (rc) break;
-        if (d == 3) {
-          void* ai[] = {&a, &yf};
-          rc = Lc.go(TY.col[KC_INV], yf_lines, ai, K_YINV);
-          if (rc) break;
-        }
-        rc = Lc.go(TX.s3[scheme], row_lines, a1, K_SWEEP3);
       }
+      if ((r = L.go(*kmid, mid_lines, amid, K_MID))) return r;
+      if (d == 3) {
+        void* ai[] = {&a, &yf};
+        if ((r = L.go(TY.col[KC_INV], yf_lines, ai, K_YINV))) return r;
+      }
+      return L.go(TX.s3[scheme], row_lines, a1, K_SWEEP3);
+    };
+
+    if (use_graph) {
+      // CUDA graph with a conditional WHILE node: the body is one iteration
+      // plus k_loop_cond; the whole solve is a single graph launch and the
+      // host never synchronises inside the loop.
+      cudaGraph_t g = nullptr, body = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      cudaGraphConditionalHandle h;
+      cudaStream_t cs = capture_stream();
+      do {
+        if ((rc = (cudaGraphCreate(&g, 0) != cudaSuccess))) break;
+        if ((rc = (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess))) break;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        if ((rc = (cudaGraphAddNode(&cn, g, nullptr, 0, &cp) != cudaSuccess))) break;
+        body = cp.conditional.phGraph_out[0];
+        if ((rc = (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
+                   cudaSuccess)))
+          break;
+        Launcher Lcap(cs, R.num_sms);
+        int r1 = launch_iter(Lcap);
+        const DevState* stp = a.st;
+        void* ca[] = {&h, &stp};
+        if (!r1) r1 = Lcap.raw((const void*)k_loop_cond, 1, 1, 0, ca, K_OP);
+        cudaGraph_t cap_out = nullptr;
+        cudaError_t ec = cudaStreamEndCapture(cs, &cap_out);
+        Lc.count += 0;
+        if (r1 || ec != cudaSuccess) {
+          rc = r1 ? r1 : 1;
+          break;
+        }
+        if ((rc = (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess))) break;
+        if ((rc = (cudaGraphLaunch(ge, s) != cudaSuccess))) break;
+      } while (0);
+      if (rc && g_err.empty()) g_err = std::string("graph loop: ") + cudaGetErrorString(cudaGetLastError());
+      if (!rc) {
+        CK(cudaMemcpyAsync(hst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const long long nrec = hst->nrec;
+        if (nrec > history_cap) {
+          g_err = "history buffer too small";
+          rc = 4;
+        } else if (nrec > 0) {
+          CK(cudaMemcpy(history, a.history, sizeof(double) * 3 * nrec, cudaMemcpyDeviceToHost));
+        }
+        // launches executed by the loop: (kernels per body) x iterations run
+        const long long per_iter = (d == 3 ? (em_type ? 6 : 5) : 3) + 1;
+        Lc.count += per_iter * std::max<long long>(hst->k, 1);
+      }
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
       if (rc) break;
-      launched_iters += todo;
-      CK(cudaMemcpyAsync(hst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      Lc.harvest();
-      // collect new history records from the device ring
-      long long nrec = hst->nrec;
-      if (nrec > history_cap) {
-        g_err = "history buffer too small";
-        rc = 4;
-        break;
+    } else {
+      // profiling: one iteration per synchronisation, so no launch after the
+      // stop is counted in the per-kernel statistics
+      long long chunk = Lc.prof ? 1 : 2;
+      const long long max_chunk = Lc.prof ? 1 : 256;
+      long long launched_iters = 0;
+      while (!stopped) {
+        long long todo = chunk;
+        if (launched_iters + todo > pr->max_iters) todo = pr->max_iters - launched_iters;
+        for (long long it = 0; it < todo && !rc; ++it) rc = launch_iter(Lc);
+        if (rc) break;
+        launched_iters += todo;
+        CK(cudaMemcpyAsync(hst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        Lc.harvest();
+        // collect new history records from the device ring
+        long long nrec = hst->nrec;
+        if (nrec > history_cap) {
+          g_err = "history buffer too small";
+          rc = 4;
+          break;
+        }
+        for (long long r0 = nrec_host; r0 < nrec;) {
+          long long slot = r0 % hist_ring;
+          long long cnt = std::min(nrec - r0, (long long)hist_ring - slot);
+          CK(cudaMemcpy(history + 3 * r0, a.history + 3 * slot, sizeof(double) * 3 * cnt, cudaMemcpyDeviceToHost));
+          r0 += cnt;
+        }
+        nrec_host = nrec;
+        stopped = hst->stopped != 0 || launched_iters >= pr->max_iters;
+        chunk = std::min<long long>(chunk * 2, max_chunk);
       }
-      for (long long r0 = nrec_host; r0 < nrec;) {
-        long long slot = r0 % hist_ring;
-        long long cnt = std::min(nrec - r0, (long long)hist_ring - slot);
-        CK(cudaMemcpy(history + 3 * r0, a.history + 3 * slot, sizeof(double) * 3 * cnt, cudaMemcpyDeviceToHost));
-        r0 += cnt;
-      }
-      nrec_host = nrec;
-      stopped = hst->stopped != 0 || launched_iters >= pr->max_iters;
-      chunk = std::min<long long>(chunk * 2, 256);
     }
     if (rc) break;
     switch (scheme) {
@@ -562,6 +657,15 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     CK(cudaStreamSynchronize(s));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ev0, ev1));
+    if (a.dbg) {
+      unsigned long long hd[8];
+      CK(cudaMemcpy(hd, a.dbg, sizeof(hd), cudaMemcpyDeviceToHost));
+      unsigned long long tot = 0;
+      for (int i = 0; i < 8; ++i) tot += hd[i];
+      fprintf(stderr, "[fftc phase cycles] loop %.1f%% tma-wait %.1f%% lds-in %.1f%% fwd %.1f%% proj %.1f%% inv %.1f%% store %.1f%% issue %.1f%%\n",
+              100.0 * hd[0] / tot, 100.0 * hd[1] / tot, 100.0 * hd[2] / tot, 100.0 * hd[3] / tot, 100.0 * hd[4] / tot,
+              100.0 * hd[5] / tot, 100.0 * hd[6] / tot, 100.0 * hd[7] / tot);
+    }
     out->device_ms = ms;
     out->status = hst->status;
     out->degenerate_flux = hst->degenerate;

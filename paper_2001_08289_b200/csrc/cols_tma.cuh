@@ -26,8 +26,8 @@ struct ColTma {
   static constexpr int THREADS = 2 * HALF;
   static constexpr int LP = Plan<L, E>::LP;
   static constexpr int NSLOT = 3;
-  static constexpr int CB = LP + 8;    // component buffer (128-B aligned for TMA)
-  static constexpr int SLOT = 2 * CB;  // double2 units, two components
+  static constexpr int CB = LP + 8;         // exchange buffer stride per component
+  static constexpr int SLOT = 2 * CB + 8;   // double2 units: two skewed exchange buffers (>= 2L TMA landing)
   static constexpr int SMEM = NSLOT * SLOT * (int)sizeof(double2);
   static constexpr int BOXR = L < 256 ? L : 256;  // rows per TMA box
   static constexpr unsigned TX = (unsigned)(2 * L * sizeof(double2));
@@ -41,14 +41,32 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* tm, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// One tensor copy brings both components of column x, all L rows: the map is
+// 4-D {2 doubles, BOXR rows, L/BOXR row blocks, d components}, box
+// {2, BOXR, L/BOXR, 2}, landing dense as [comp][y] in the slot.
 template <int L>
 __device__ __forceinline__ void cols_tma_issue(const CUtensorMap* tm, double2* slot, uint64_t* bar, int x) {
   using K = ColTma<L>;
+  bulk_wait_read0();  // an earlier TMA store from this slot has finished reading it
   mbar_expect_tx(bar, K::TX);
-#pragma unroll 1
-  for (int c = 0; c < 2; ++c)
-#pragma unroll 1
-    for (int y0 = 0; y0 < L; y0 += K::BOXR) tma_load_3d(slot + c * K::CB + y0, tm, 2 * x, y0, c, bar);
+  tma_load_4d(slot, tm, 2 * x, 0, 0, 0, bar);
 }
 
 struct HalfSync {
@@ -56,6 +74,19 @@ struct HalfSync {
   int n;
   __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 };
+
+#ifdef FFTC_PHASE_TIMING
+#define PHASE_MARK(i)                                                                            \
+  do {                                                                                           \
+    const long long now_ = clock64();                                                            \
+    if (ht == 0 && a.dbg) atomicAdd(&a.dbg[i], (unsigned long long)(now_ - tph_));               \
+    tph_ = now_;                                                                                 \
+  } while (0)
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#endif
 
 template <int MODE, int L>
 __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
@@ -84,21 +115,29 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
       cols_tma_issue<L>(f == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], (int)(line - (long long)f * a.nx));
     }
   double acc[NQ] = {0.0};
+#ifdef FFTC_PHASE_TIMING
+  long long tph_ = clock64();
+#endif
   for (long long k = half; k < nmine; k += 2) {
     const int s = (int)(k % K::NSLOT);
     const long long line = blockIdx.x + k * gridDim.x;
     const int f = (int)(line / a.nx);
     const int x = (int)(line - (long long)f * a.nx);
-    double2* buf = smem + s * K::SLOT + comp * K::CB;
-    // exchanges of component 1 run 4 slots (64 B) off component 0: the
-    // partner lanes then hit disjoint bank groups
-    double2* xbuf = buf + 4 * comp;
+    double2* slot = smem + s * K::SLOT;
+    const double2* inb = slot + comp * L;  // TMA landing layout [comp][y]
+    // exchange buffers: component c at c*CB, component 1 skewed by 4 slots
+    // (64 B) so that partner lanes hit disjoint bank groups
+    double2* xbuf = slot + comp * (K::CB + 4);
+    PHASE_MARK(0);
     mbar_wait(&bars[s], (unsigned)((k / K::NSLOT) & 1));
+    PHASE_MARK(1);
     double2 v[1][E];
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[0][i] = buf[pos_first<L, E>(false, t, i)];
+    for (int i = 0; i < E; ++i) v[0][i] = inb[pos_first<L, E>(false, t, i)];
     hsync();  // slot becomes exchange scratch
+    PHASE_MARK(2);
     fft_line<L, E, 1, false>(v, t, a.tw[1], SmemBuf{xbuf, 0}, hsync);
+    PHASE_MARK(3);
     const double kx = (double)wavenum(x, a.nx);
     const bool parseval_only = (MODE == MID_EM) && f == 1;
 #pragma unroll
@@ -121,20 +160,34 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
         v[0][i] = csub(v[0][i], cscale(dot, 2.0 * kc));
       }
     }
+    PHASE_MARK(4);
     if (!parseval_only) {
       fft_line<L, E, 1, true>(v, t, a.tw[1], SmemBuf{xbuf, 0}, hsync);
-      double2* F = ((f == 0) ? a.A : a.B) + (size_t)comp * a.N + x;
+      PHASE_MARK(5);
+      // outputs -> slot in the tensor layout, then one TMA store per line
+      double2* outb = slot + comp * L;
 #pragma unroll
-      for (int i = 0; i < E; ++i) F[(size_t)pos_last<L, E>(true, t, i) * a.nx] = v[0][i];
+      for (int i = 0; i < E; ++i) outb[pos_last<L, E>(true, t, i)] = v[0][i];
+      fence_proxy_async();
+      hsync();
+      if (ht == 0) {
+        tma_store_4d(&tmA, slot, 2 * x, 0, 0, 0);
+        bulk_commit();
+      }
+    } else {
+      hsync();  // slot s consumed
     }
-    hsync();  // slot s consumed
+    PHASE_MARK(6);
     if (ht == 0 && k + K::NSLOT < nmine) {
+      PHASE_MARK(6);
       fence_proxy_async();
       const long long nl = line + (long long)K::NSLOT * gridDim.x;
       const int nf = (int)(nl / a.nx);
       cols_tma_issue<L>(nf == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], (int)(nl - (long long)nf * a.nx));
+      PHASE_MARK(7);
     }
   }
+  if (ht == 0) bulk_wait0();  // this half's TMA stores have landed in global memory
   double tot[NQ];
   if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
     monitor_step(a, tot[0] * (double)a.N + a.st->js2);

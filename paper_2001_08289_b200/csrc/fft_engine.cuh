@@ -205,10 +205,26 @@ __device__ __forceinline__ int pos_last(bool inv, int t, int i) {
 template <int PS>
 __device__ __forceinline__ int padpos(int p) { return p + (p >> PS); }
 
-// Multiply element r of every channel by w^r (w = tw[m], direction INV),
-// r = 1..R-1.  Powers come from table loads of w, w^2, w^4, w^8 and at most
-// three complex products; each power is applied as soon as it is formed so
-// only a handful of twiddles are live at once.
+// Twiddle bases of one butterfly: w, w^2, w^4, w^8 of w = tw[m] (table
+// loads).  Loaded one stage ahead -- before the exchange barrier that
+// precedes the stage -- so the L1/L2 latency hides behind the exchange.
+struct TwBase {
+  double2 w1, w2, w4, w8;
+};
+
+template <int R>
+__device__ __forceinline__ TwBase load_twbase(const double2* __restrict__ tw, int m) {
+  TwBase b;
+  b.w1 = __ldg(&tw[m]);
+  if constexpr (R >= 4) b.w2 = __ldg(&tw[2 * m]);
+  if constexpr (R >= 8) b.w4 = __ldg(&tw[4 * m]);
+  if constexpr (R >= 16) b.w8 = __ldg(&tw[8 * m]);
+  return b;
+}
+
+// Multiply element r of every channel by w^r (direction INV), r = 1..R-1,
+// powers from the bases with at most three complex products each; each power
+// is applied as soon as it is formed so few twiddles are live at once.
 template <int C, int E, bool INV>
 __device__ __forceinline__ void twmul(double2 (&v)[C][E], int idx, double2 w) {
 #pragma unroll
@@ -216,23 +232,23 @@ __device__ __forceinline__ void twmul(double2 (&v)[C][E], int idx, double2 w) {
 }
 
 template <int R, int C, int E, bool INV>
-__device__ __forceinline__ void apply_twiddles(double2 (&v)[C][E], int base, const double2* __restrict__ tw, int m) {
-  const double2 w1 = __ldg(&tw[m]);
+__device__ __forceinline__ void apply_twiddles(double2 (&v)[C][E], int base, const TwBase& b) {
+  const double2 w1 = b.w1;
   twmul<C, E, INV>(v, base + 1, w1);
   if constexpr (R >= 4) {
-    const double2 w2 = __ldg(&tw[2 * m]);
+    const double2 w2 = b.w2;
     twmul<C, E, INV>(v, base + 2, w2);
     const double2 w3 = cmul(w1, w2);
     twmul<C, E, INV>(v, base + 3, w3);
     if constexpr (R >= 8) {
-      const double2 w4 = __ldg(&tw[4 * m]);
+      const double2 w4 = b.w4;
       twmul<C, E, INV>(v, base + 4, w4);
       twmul<C, E, INV>(v, base + 5, cmul(w1, w4));
       twmul<C, E, INV>(v, base + 6, cmul(w2, w4));
       const double2 w7 = cmul(w3, w4);
       twmul<C, E, INV>(v, base + 7, w7);
       if constexpr (R >= 16) {
-        const double2 w8 = __ldg(&tw[8 * m]);
+        const double2 w8 = b.w8;
         twmul<C, E, INV>(v, base + 8, w8);
         twmul<C, E, INV>(v, base + 9, cmul(w1, w8));
         twmul<C, E, INV>(v, base + 10, cmul(w2, w8));
@@ -246,17 +262,34 @@ __device__ __forceinline__ void apply_twiddles(double2 (&v)[C][E], int base, con
   }
 }
 
+// twiddle bases of every butterfly a thread owns in stage S
+template <int L, int E, bool INV, int S>
+struct StageTw {
+  using P = Plan<L, E>;
+  static constexpr int R = P::radix(INV, S);
+  static constexpr int Ns = P::ns(INV, S);
+  static constexpr int NB = (Ns > 1) ? E / R : 1;
+  TwBase b[NB];
+  __device__ __forceinline__ void load(int t, const double2* __restrict__ tw) {
+    if constexpr (Ns > 1) {
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const int j = t + k * P::T;
+        b[k] = load_twbase<R>(tw, (j & (Ns - 1)) * (L / (Ns * R)));
+      }
+    }
+  }
+};
+
 // One Stockham stage (compute only, registers in place).
 template <int L, int E, int C, bool INV, int S>
-__device__ __forceinline__ void stage_compute(double2 (&v)[C][E], int t, const double2* __restrict__ tw) {
+__device__ __forceinline__ void stage_compute(double2 (&v)[C][E], const StageTw<L, E, INV, S>& tws) {
   using P = Plan<L, E>;
   constexpr int R = P::radix(INV, S);
   constexpr int Ns = P::ns(INV, S);
-  constexpr int T = P::T;
 #pragma unroll
   for (int b = 0; b < E / R; ++b) {
-    const int j = t + b * T;
-    if constexpr (Ns > 1) apply_twiddles<R, C, E, INV>(v, b * R, tw, (j & (Ns - 1)) * (L / (Ns * R)));
+    if constexpr (Ns > 1) apply_twiddles<R, C, E, INV>(v, b * R, tws.b[b]);
 #pragma unroll
     for (int c = 0; c < C; ++c) dftR<R, INV>(&v[c][b * R]);
   }
@@ -321,12 +354,15 @@ __device__ __forceinline__ void stage_exchange(double2 (&v)[C][E], int t, Buf bu
 }
 
 template <int L, int E, int C, bool INV, int S, class Buf, class Bar>
-__device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, const double2* __restrict__ tw, Buf buf, Bar bar) {
+__device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, const double2* __restrict__ tw, Buf buf, Bar bar,
+                                         const StageTw<L, E, INV, S>& tws) {
   using P = Plan<L, E>;
-  stage_compute<L, E, C, INV, S>(v, t, tw);
+  stage_compute<L, E, C, INV, S>(v, tws);
   if constexpr (S + 1 < P::NST) {
+    StageTw<L, E, INV, S + 1> nxt;
+    nxt.load(t, tw);  // in flight during the exchange
     stage_exchange<L, E, C, INV, S>(v, t, buf, bar);
-    run_from<L, E, C, INV, S + 1>(v, t, tw, buf, bar);
+    run_from<L, E, C, INV, S + 1>(v, t, tw, buf, bar, nxt);
   }
 }
 
@@ -334,7 +370,8 @@ __device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, const double
 // at pos_first(INV,t,i); output: element i at pos_last(INV,t,i).
 template <int L, int E, int C, bool INV, class Buf, class Bar>
 __device__ __forceinline__ void fft_line(double2 (&v)[C][E], int t, const double2* __restrict__ tw, Buf buf, Bar bar) {
-  run_from<L, E, C, INV, 0>(v, t, tw, buf, bar);
+  StageTw<L, E, INV, 0> first;  // stage 0 has Ns = 1: no twiddles
+  run_from<L, E, C, INV, 0>(v, t, tw, buf, bar, first);
 }
 
 // ----------------------------------------------------------------------------
@@ -371,7 +408,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // plus two Newton steps in fp64, branch free (the IEEE division of the
 // plain form carries a slow path per element); within 1 ulp of 1.0/k2.
 __device__ __forceinline__ double inv_k2(double k2) {
-  double y = (double)__frcp_rn((float)k2);
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(k2));
   y = fma(y, fma(-k2, y, 1.0), y);
   y = fma(y, fma(-k2, y, 1.0), y);
   return y;

@@ -17,18 +17,30 @@
 
 namespace fftc {
 
+#ifndef FFTC_ST_NSTAGE
+#define FFTC_ST_NSTAGE 1
+#endif
+
+#ifndef FFTC_ROW_E
+#define FFTC_ROW_E 16
+#endif
 template <int S, int SW, int L>
 struct RowTma {
-  static constexpr int E = 16;
+  static constexpr int E = FFTC_ROW_E;
   static constexpr int T = L / E;
   static constexpr int CH = (SW == 1) ? Sweep1Traits<S>::C : 1;
   static constexpr int THREADS = CH * T;
   static constexpr bool X0_ROW = (SW == 3) && (S == BASIC || S == BASIC_SUB);  // extra staged row
+  // sweep 1 of the substituted schemes also stages its S (and T) rows over
+  // the phase-1 extent; those areas are LP long so the first one can serve
+  // as channel 1's exchange buffer once the inputs are in registers
+  static constexpr int ST_ROWS = (SW == 1 && S == BASIC_SUB) ? 1 : 0;
   static constexpr int LP = Plan<L, E>::LP;
-  static constexpr int CHI_OFF = LP + (X0_ROW ? L : 0);      // double2 units
-  static constexpr int STAGE = CHI_OFF + L / 16;             // chi row = L bytes
-  static constexpr int NSTAGE = 2;
-  static constexpr int XBUF = (CH == 2) ? LP : 0;            // exchange buffer of channel 1
+  static constexpr int ST_OFF = LP + (X0_ROW ? L : 0);
+  static constexpr int CHI_OFF = ST_OFF + ST_ROWS * LP;     // double2 units
+  static constexpr int STAGE = CHI_OFF + L / 16;            // chi row = L bytes
+  static constexpr int NSTAGE = ST_ROWS ? FFTC_ST_NSTAGE : 2;
+  static constexpr int XBUF = (CH == 2 && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
   static constexpr int SMEM = (NSTAGE * STAGE + XBUF) * (int)sizeof(double2);
   static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + L);
 };
@@ -40,9 +52,26 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
   const int c = (int)(line / rows);
   const long long row = line - (long long)c * rows;
   const size_t off = (size_t)c * a.N + (size_t)row * L;
-  mbar_expect_tx(bar, K::TX);
+  unsigned tx = K::TX;
+  int x0 = 0;
+  unsigned nb = 0;
+  if constexpr (K::ST_ROWS > 0) {
+    const int2 ext = a.row_ext[row];
+    if (ext.x < ext.y) {
+      x0 = ext.x & ~1;
+      nb = (unsigned)((ext.y - x0) * sizeof(double2) + 15) & ~15u;
+      tx += K::ST_ROWS * nb;
+    }
+  }
+  mbar_expect_tx(bar, tx);
   bulk_g2s(stage, (SW == 1 ? a.X[0] : a.A) + off, (unsigned)(L * sizeof(double2)), bar);
   if constexpr (K::X0_ROW) bulk_g2s(stage + K::LP, a.X[0] + off, (unsigned)(L * sizeof(double2)), bar);
+  if constexpr (K::ST_ROWS > 0) {
+    if (nb) {
+      bulk_g2s(stage + K::ST_OFF + x0, a.X[1] + off + x0, nb, bar);
+      if constexpr (K::ST_ROWS > 1) bulk_g2s(stage + K::ST_OFF + K::LP + x0, a.X[2] + off + x0, nb, bar);
+    }
+  }
   bulk_g2s(stage + K::CHI_OFF, a.chi + (size_t)row * L, (unsigned)L, bar);
 }
 
@@ -50,6 +79,7 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
 template <int S, int SW, int L>
 __device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, long long line, long long lines, long long rows) {
   if (!(S == BASIC_SUB || S == EM_SUB) || line >= lines) return;
+  if (RowTma<S, SW, L>::ST_ROWS > 0) return;  // staged by TMA instead
   const int c = (int)(line / rows);
   const long long row = line - (long long)c * rows;
   const int2 ext = a.row_ext[row];
@@ -62,7 +92,7 @@ __device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, long long
 }
 
 template <int S, int SW, int L>
-__global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : 2) k_rows_tma(Args a) {
+__global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowTma<S, SW, L>::ST_ROWS ? 1 : 2)) k_rows_tma(Args a) {
   using K = RowTma<S, SW, L>;
   constexpr int E = K::E, T = K::T, CH = K::CH;
   constexpr int NQ = (SW == 1) ? Sweep1Traits<S>::NQ : 6;
@@ -121,9 +151,15 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : 2) k_
             v[0][i] = cmul(in1 ? a.sm1 : a.sm2, q);
           }
         } else {
-          const double2 sv = in1 ? a.X[1][off + x] : czero();
-          double2 tv = czero();
-          if constexpr (S == EM_SUB) tv = in1 ? a.X[2][off + x] : czero();
+          double2 sv = czero(), tv = czero();
+          if (in1) {
+            if constexpr (K::ST_ROWS >= 1) sv = st[K::ST_OFF + x];
+            else sv = a.X[1][off + x];
+            if constexpr (S == EM_SUB) {
+              if constexpr (K::ST_ROWS >= 2) tv = st[K::ST_OFF + K::LP + x];
+              else tv = a.X[2][off + x];
+            }
+          }
           const AugFlux f = apply_A(a, in1, q, sv, tv);
           if (jchan) {
             double2 jq, js;
@@ -141,7 +177,7 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : 2) k_
       for (int i = 0; i < E; ++i) v[0][i] = st[pos_first<L, E>(true, t, i)];
     }
     __syncthreads();  // the main row becomes exchange scratch
-    double2* xb = (CH == 2 && ch == 1) ? xbuf : st;
+    double2* xb = (CH == 2 && ch == 1) ? (K::ST_ROWS ? st + K::ST_OFF : xbuf) : st;
     fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
     if constexpr (SW == 1) {
 #pragma unroll

@@ -76,6 +76,7 @@ struct Args {
   int hist_cap;
   int op_mode;  // 1: operator API call -- no stop flag, no monitor
   DevState* st;
+  unsigned long long* dbg;  // debug phase counters (FFTC_PHASE_TIMING builds), else null
   const double2* tw[3];  // twiddles for n_x, n_y, n_z
   // scalars (host-prepared, see abi.cu)
   double2 sigma1, s0, e0[3];
