@@ -89,6 +89,40 @@ int fftc_solve(const fftc_problem* problem, const fftc_params* params, double* h
 int fftc_solve_batch(const fftc_problem* problem, const fftc_params* params, int32_t n_points,
                      double* histories, int64_t history_cap, fftc_result* out, void* stream);
 
+/* z-slab decomposition of a 3-D solve over `world` ranks (BASELINE config 4,
+ * north star: "slab-decomposed across the 8 GPUs ... NCCL all-to-all FFT
+ * transposes").  Rank r owns z-planes [z0, z0+nzl) of the state and of the
+ * work fields A_z/B_z (layout (c, z_l, y, x)); the z pass runs on a y-slab
+ * copy A_y/B_y (layout (c, y_l, z, x), y-planes [y0, y0+nyl)) that the caller
+ * produces with an all-to-all transpose after FFTC_SLAB_ROWS_FWD and
+ * transposes back (A only) after FFTC_SLAB_MID.  Every phase returns
+ * rank-local partial sums the caller all-reduces:
+ *   INIT     -> out[6]  e0 - (local sum of the initial iterate)/N   (per component re, im)
+ *   ROWS_FWD -> out[7]  local <j> contribution (6) and sum |Js|^2 chi (1)
+ *   MID      -> out[1]  local sum_x |Gamma j|^2
+ *   ROWS_INV -> out[6]  as INIT for the new iterate
+ * The caller forms the global delta = sum_r out_r - (world-1) e0 and installs
+ * it with fftc_slab_set_delta; fftc_slab_monitor runs the reference stopping
+ * rule (solvers.py:243-277) on the global totals {<j> (6), js2, parseval} and
+ * returns {stopped, status, degenerate, nrec, sigma*_re, sigma*_im, residual}. */
+enum { FFTC_SLAB_INIT = 0, FFTC_SLAB_ROWS_FWD = 1, FFTC_SLAB_MID = 2, FFTC_SLAB_ROWS_INV = 3 };
+typedef struct fftc_slab_desc {
+  int32_t d;          /* 3 */
+  int32_t reserved;
+  int64_t n[3];       /* GLOBAL nx, ny, nz */
+  int64_t z0, nzl;    /* this rank's z-slab */
+  int64_t y0, nyl;    /* this rank's y-slab after the transpose */
+  const uint8_t* chi; /* DEVICE, local z-slab of the indicator (nzl*ny*nx bytes) */
+} fftc_slab_desc;
+typedef struct fftc_slab fftc_slab;
+int fftc_slab_create(const fftc_slab_desc* desc, const fftc_params* params, void* A_z, void* B_z, void* A_y,
+                     void* B_y, fftc_slab** out, void* stream);
+int fftc_slab_phase(fftc_slab* slab, int32_t phase, double* out, void* stream);
+int fftc_slab_set_delta(fftc_slab* slab, const double* delta6, void* stream);
+int fftc_slab_monitor(fftc_slab* slab, const double* totals8, double* record7, void* stream);
+int fftc_slab_finalize(fftc_slab* slab, void* E, void* J, void* aug, double* means12, void* stream);
+void fftc_slab_destroy(fftc_slab* slab);
+
 /* Same contract, host-resident chi and outputs (the library copies in and
  * out; E/J/aug host buffers are nullable).  For FFI users without a device
  * allocator. */

@@ -199,6 +199,48 @@ double2 hdiv(double2 a, double2 b) {
   return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
 }
 
+// Scalars of one solve (host side, mirroring the reference expressions:
+// solvers.py:286-290, :369-392); the grid fields are filled by the caller.
+void fill_scalars(Args& a, const fftc_params* pr, int d, long long N) {
+  const double2 one = make_double2(1.0, 0.0);
+  a.sigma1 = C2(pr->sigma1);
+  a.s0 = C2(pr->sigma0);
+  double e0sq = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    a.e0[c] = c < d ? C2(pr->e0[c]) : make_double2(0, 0);
+    e0sq += a.e0[c].x * a.e0[c].x + a.e0[c].y * a.e0[c].y;
+  }
+  a.e0sq = e0sq;
+  a.tol = pr->tol;
+  a.inv_n = 1.0 / (double)N;
+  a.gscale = pr->gamma1_scale;
+  a.max_iters = pr->max_iters;
+  a.inv_s0 = hinv(a.s0);
+  a.sum1 = hadd(a.sigma1, a.s0);
+  a.sum2 = hadd(one, a.s0);
+  a.inv_sum1 = hinv(a.sum1);
+  a.inv_sum2 = hinv(a.sum2);
+  a.sm1 = hsub(a.sigma1, a.s0);
+  a.sm2 = hsub(one, a.s0);
+  const double2 two_s0 = make_double2(2.0 * a.s0.x, 2.0 * a.s0.y);
+  for (int c = 0; c < 3; ++c) a.two_s0_e0[c] = hmul(two_s0, a.e0[c]);
+  const double2 t = C2(pr->t);
+  a.p1 = C2(pr->p1);
+  a.p2 = C2(pr->p2);
+  a.p3 = C2(pr->p3);
+  const double2 tm1 = hsub(t, one);
+  a.tm1p1 = hmul(tm1, a.p1);
+  a.tm1p2 = hmul(tm1, a.p2);
+  a.tm1p3 = hmul(tm1, a.p3);
+  a.cq = hmul(a.p1, a.tm1p1);
+  a.cs = hmul(a.p2, a.tm1p1);
+  a.sinv = hdiv(one, hadd(one, a.s0));            // inv_scale = 1/(1+s0)   (solvers.py:388)
+  const double2 cinv = hdiv(tm1, hadd(t, a.s0));  // inv_c = (t-1)/(t+s0)  (solvers.py:389)
+  a.cinv_p1 = hmul(cinv, a.p1);
+  a.cinv_p2 = hmul(cinv, a.p2);
+  a.cinv_p3 = hmul(cinv, a.p3);
+}
+
 // ---- optional per-kernel timing (fftc_profile): event pairs per launch ----
 enum KindId { K_SWEEP1 = 0, K_MID, K_SWEEP3, K_YFWD, K_YINV, K_INIT, K_FINAL, K_OP, K_NKIND };
 const char* kKindName[K_NKIND] = {"sweep1_rows_fwd", "sweep2_cols_gamma", "sweep3_rows_inv", "y_fwd_3d",
@@ -310,6 +352,18 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const DevState* st) {
   cudaGraphSetConditional(h, st->stopped ? 0u : 1u);
 }
 
+// distributed solve: install global totals, then run the stopping monitor
+__global__ void k_dist_monitor(Args a, const double* __restrict__ tot) {
+  if (threadIdx.x || blockIdx.x) return;
+  for (int c = 0; c < a.d; ++c) a.st->jmean[c] = make_double2(tot[2 * c], tot[2 * c + 1]);
+  a.st->js2 = tot[6];
+  monitor_step(a, tot[7] + tot[6]);
+}
+__global__ void k_dist_set_delta(Args a, const double* __restrict__ dl) {
+  if (threadIdx.x || blockIdx.x) return;
+  for (int c = 0; c < a.d; ++c) a.st->delta[c] = make_double2(dl[2 * c], dl[2 * c + 1]);
+}
+
 cudaStream_t capture_stream() {
   thread_local cudaStream_t cs = nullptr;
   if (!cs) cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
@@ -382,43 +436,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   a.nz = (int)nz;
   a.N = N;
   a.chi = pb->chi;
-  a.sigma1 = C2(pr->sigma1);
-  a.s0 = C2(pr->sigma0);
-  double e0sq = 0.0;
-  for (int c = 0; c < 3; ++c) {
-    a.e0[c] = c < d ? C2(pr->e0[c]) : make_double2(0, 0);
-    e0sq += a.e0[c].x * a.e0[c].x + a.e0[c].y * a.e0[c].y;
-  }
-  a.e0sq = e0sq;
-  a.tol = pr->tol;
-  a.inv_n = 1.0 / (double)N;
-  a.gscale = pr->gamma1_scale;
-  a.max_iters = pr->max_iters;
-  const double2 one = make_double2(1.0, 0.0);
-  a.inv_s0 = hinv(a.s0);
-  a.sum1 = hadd(a.sigma1, a.s0);
-  a.sum2 = hadd(one, a.s0);
-  a.inv_sum1 = hinv(a.sum1);
-  a.inv_sum2 = hinv(a.sum2);
-  a.sm1 = hsub(a.sigma1, a.s0);
-  a.sm2 = hsub(one, a.s0);
-  const double2 two_s0 = make_double2(2.0 * a.s0.x, 2.0 * a.s0.y);
-  for (int c = 0; c < 3; ++c) a.two_s0_e0[c] = hmul(two_s0, a.e0[c]);
-  const double2 t = C2(pr->t);
-  a.p1 = C2(pr->p1);
-  a.p2 = C2(pr->p2);
-  a.p3 = C2(pr->p3);
-  const double2 tm1 = hsub(t, one);
-  a.tm1p1 = hmul(tm1, a.p1);
-  a.tm1p2 = hmul(tm1, a.p2);
-  a.tm1p3 = hmul(tm1, a.p3);
-  a.cq = hmul(a.p1, a.tm1p1);
-  a.cs = hmul(a.p2, a.tm1p1);
-  a.sinv = hdiv(one, hadd(one, a.s0));         // inv_scale = 1/(1+s0)   (solvers.py:388)
-  const double2 cinv = hdiv(tm1, hadd(t, a.s0));  // inv_c = (t-1)/(t+s0)  (solvers.py:389)
-  a.cinv_p1 = hmul(cinv, a.p1);
-  a.cinv_p2 = hmul(cinv, a.p2);
-  a.cinv_p3 = hmul(cinv, a.p3);
+  fill_scalars(a, pr, d, N);
 
   // ---- workspace ----
   const int nslots = scheme == FFTC_EM_SUB ? 3 : (scheme == FFTC_BASIC_SUB ? 2 : 1);
@@ -516,6 +534,8 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       mid.stride = nx * ny;
       mid.ostride = nx;
       mid.nstrips = (int)(nx / TZ.col3_w);
+      mid.o0 = 0;
+      mid.on = (int)ny;
       kmid = &TZ.col[em_type ? KC_MID3_EM : KC_MID3_BASIC];
       yf.axis = 1;
       yf.nouter = (int)nz;
@@ -850,6 +870,8 @@ int fftc_gamma1(const fftc_problem* pb, const void* in, void* out, double scale,
       mid.stride = g.nx * g.ny;
       mid.ostride = g.nx;
       mid.nstrips = (int)(g.nx / R.tab[g.lgz].col3_w);
+      mid.o0 = 0;
+      mid.on = (int)g.ny;
       kmid = &R.tab[g.lgz].col[KC_MID3_BASIC];
     }
     void* args[] = {&a, &mid};
@@ -904,6 +926,8 @@ int fftc_debug_project(const fftc_problem* pb, void* data, void* stream) {
     mid.stride = g.nx * g.ny;
     mid.ostride = g.nx;
     mid.nstrips = (int)(g.nx / R.tab[g.lgz].col3_w);
+    mid.o0 = 0;
+    mid.on = (int)g.ny;
     kmid = &R.tab[g.lgz].col[KC_MID3_BASIC];
   }
   void* args[] = {&a, &mid};
@@ -931,6 +955,274 @@ int fftc_solve_batch(const fftc_problem* pb, const fftc_params* params, int32_t 
     }
   }
   return 0;
+}
+
+// ---------------------------------------------------------------------------
+// z-slab decomposition (BASELINE config 4): one rank per GPU owns z-planes
+// [z0, z0 + nzl) of the state and work fields; the z pass runs on a y-slab
+// copy [y0, y0 + nyl) produced by the caller's all-to-all transpose.  Every
+// reduction leaves a rank-local partial that the caller all-reduces.
+// ---------------------------------------------------------------------------
+struct fftc_slab {
+  Args row;     // z-slab geometry (local nz), work fields A_z / B_z
+  Args mid;     // y-slab geometry (global nz), work fields A_y / B_y
+  ColGeom yf{}, zg{};
+  int scheme = 0, lgx = 0, lgy = 0, lgz = 0;
+  bool em_type = false;
+  long long N_l = 0;
+  char* ws = nullptr;
+  double* tot_dev = nullptr;  // 8 doubles of host-supplied totals
+  DevState* hst = nullptr;
+};
+
+int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, void* Bz, void* Ay, void* By,
+                     fftc_slab** out, void* stream) {
+  g_err.clear();
+  if (!sd || !pr || !out || sd->d != 3) {
+    g_err = "slab: d must be 3";
+    return 2;
+  }
+  const long long nx = sd->n[0], ny = sd->n[1], nz = sd->n[2];
+  const int lgx = lg2_exact(nx), lgy = lg2_exact(ny), lgz = lg2_exact(nz);
+  if (lgx < 0 || lgy < 0 || lgz < 0 || sd->nzl < 1 || sd->nyl < 1 || sd->nzl * ny != sd->nyl * nz) {
+    g_err = "slab: unsupported grid or inconsistent slabs";
+    return 3;
+  }
+  if (ensure_registry()) return 1;
+  Registry& R = reg();
+  cudaStream_t s = (cudaStream_t)stream;
+  fftc_slab* sl = new fftc_slab();
+  const int d = 3;
+  const long long N_l = nx * ny * sd->nzl, N_g = nx * ny * nz;
+  sl->N_l = N_l;
+  sl->scheme = pr->scheme;
+  sl->lgx = lgx;
+  sl->lgy = lgy;
+  sl->lgz = lgz;
+  sl->em_type = (pr->scheme == FFTC_EM || pr->scheme == FFTC_EM_SUB);
+  Args& a = sl->row;
+  memset(&a, 0, sizeof(a));
+  a.d = d;
+  a.nx = (int)nx;
+  a.ny = (int)ny;
+  a.nz = (int)sd->nzl;
+  a.N = N_l;
+  a.chi = sd->chi;
+  fill_scalars(a, pr, d, N_g);  // means and normalisations are global
+  a.dist = 1;
+  const int nslots = pr->scheme == FFTC_EM_SUB ? 3 : (pr->scheme == FFTC_BASIC_SUB ? 2 : 1);
+  const size_t fld = sizeof(double2) * (size_t)d * N_l;
+  const int hist_cap = (int)std::max<int64_t>(pr->max_iters, 16);
+  const size_t pc = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
+  const size_t bytes = fld * nslots + sizeof(double) * pc + sizeof(double) * 3 * hist_cap + sizeof(DevState) +
+                       sizeof(int2) * (size_t)ny * sd->nzl + sizeof(double) * 8 + 8192;
+  if (cudaMalloc((void**)&sl->ws, bytes) != cudaSuccess) {
+    g_err = "slab: workspace allocation failed";
+    delete sl;
+    return 1;
+  }
+  size_t o = 0;
+  auto carve = [&](size_t b) {
+    char* p = sl->ws + o;
+    o += (b + 255) & ~(size_t)255;
+    return p;
+  };
+  for (int i = 0; i < nslots; ++i) a.X[i] = (double2*)carve(fld);
+  a.partials = (double*)carve(sizeof(double) * pc);
+  a.history = (double*)carve(sizeof(double) * 3 * hist_cap);
+  a.hist_cap = hist_cap;
+  a.st = (DevState*)carve(sizeof(DevState));
+  a.row_ext = (const int2*)carve(sizeof(int2) * (size_t)ny * sd->nzl);
+  sl->tot_dev = (double*)carve(sizeof(double) * 8);
+  a.A = (double2*)Az;
+  a.B = sl->em_type ? (double2*)Bz : (double2*)Az;
+  a.tw[0] = R.tw[lgx];
+  a.tw[1] = R.tw[lgy];
+  a.tw[2] = R.tw[lgz];
+  sl->mid = a;
+  sl->mid.nz = (int)nz;  // the z pass sees whole z lines
+  sl->mid.A = (double2*)Ay;
+  sl->mid.B = sl->em_type ? (double2*)By : (double2*)Ay;
+  // y passes on the z-slab (lines along y, one per (z, x-strip, component))
+  sl->yf.axis = 1;
+  sl->yf.nouter = (int)sd->nzl;
+  sl->yf.stride = nx;
+  sl->yf.ostride = nx * ny;
+  sl->yf.nstrips = (int)(nx / 2);
+  // z pass on the y-slab, layout (c, y_l, z, x): lines along z, stride nx
+  sl->zg.axis = 2;
+  sl->zg.nouter = (int)sd->nyl;
+  sl->zg.stride = nx;
+  sl->zg.ostride = nz * nx;
+  sl->zg.nstrips = (int)(nx / R.tab[lgz].col3_w);
+  sl->zg.o0 = (int)sd->y0;
+  sl->zg.on = (int)ny;
+  if (cudaMallocHost((void**)&sl->hst, sizeof(DevState)) != cudaSuccess ||
+      cudaMemsetAsync(a.st, 0, sizeof(DevState), s) != cudaSuccess) {
+    g_err = "slab: state allocation failed";
+    cudaFree(sl->ws);
+    delete sl;
+    return 1;
+  }
+  *out = sl;
+  return 0;
+}
+
+static int slab_read_state(fftc_slab* sl, cudaStream_t s) {
+  CK(cudaMemcpyAsync(sl->hst, sl->row.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
+  g_err.clear();
+  Registry& R = reg();
+  cudaStream_t s = (cudaStream_t)stream;
+  Launcher Lc(s, R.num_sms);
+  Args& a = sl->row;
+  const int d = a.d;
+  const LTable& TX = R.tab[sl->lgx];
+  const LTable& TY = R.tab[sl->lgy];
+  const LTable& TZ = R.tab[sl->lgz];
+  const long long rows = (long long)a.ny * a.nz;
+  const long long yf_lines = (long long)sl->yf.nouter * sl->yf.nstrips * d;
+  int rc = 0;
+  void* a1[] = {&a};
+  switch (phase) {
+    case FFTC_SLAB_INIT: {
+      CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
+      unsigned g = (unsigned)std::min<long long>((rows + 7) / 8, (long long)R.num_sms * 8);
+      void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
+      if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) return rc;
+      switch (sl->scheme) {
+        case FFTC_BASIC: rc = launch_elementwise(k_init<BASIC>, Lc, (long long)d * a.N, a, K_INIT); break;
+        case FFTC_EM: rc = launch_elementwise(k_init<EM>, Lc, (long long)d * a.N, a, K_INIT); break;
+        case FFTC_BASIC_SUB: rc = launch_elementwise(k_init<BASIC_SUB>, Lc, (long long)d * a.N, a, K_INIT); break;
+        default: rc = launch_elementwise(k_init<EM_SUB>, Lc, (long long)d * a.N, a, K_INIT); break;
+      }
+      if (rc) return rc;
+      if (slab_read_state(sl, s)) return 1;
+      for (int c = 0; c < 3; ++c) {
+        out[2 * c] = sl->hst->delta[c].x;
+        out[2 * c + 1] = sl->hst->delta[c].y;
+      }
+      return 0;
+    }
+    case FFTC_SLAB_ROWS_FWD: {
+      if ((rc = Lc.go(TX.s1[sl->scheme], (long long)d * rows, a1, K_SWEEP1))) return rc;
+      void* ayf[] = {&a, &sl->yf};
+      if ((rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD))) return rc;
+      if (sl->em_type) {
+        Args aB = a;
+        aB.A = a.B;
+        void* ab[] = {&aB, &sl->yf};
+        if ((rc = Lc.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD))) return rc;
+      }
+      if (slab_read_state(sl, s)) return 1;
+      for (int c = 0; c < 3; ++c) {
+        out[2 * c] = sl->hst->jmean[c].x;
+        out[2 * c + 1] = sl->hst->jmean[c].y;
+      }
+      out[6] = sl->hst->js2;
+      return 0;
+    }
+    case FFTC_SLAB_MID: {
+      const KInfo& k = TZ.col[sl->em_type ? KC_MID3_EM : KC_MID3_BASIC];
+      void* am[] = {&sl->mid, &sl->zg};
+      const long long lines = (long long)sl->zg.nouter * sl->zg.nstrips * (sl->em_type ? 2 : 1);
+      if ((rc = Lc.go(k, lines, am, K_MID))) return rc;
+      if (slab_read_state(sl, s)) return 1;
+      out[0] = sl->hst->parseval;
+      return 0;
+    }
+    case FFTC_SLAB_ROWS_INV: {
+      void* ai[] = {&a, &sl->yf};
+      if ((rc = Lc.go(TY.col[KC_INV], yf_lines, ai, K_YINV))) return rc;
+      if ((rc = Lc.go(TX.s3[sl->scheme], (long long)d * rows, a1, K_SWEEP3))) return rc;
+      if (slab_read_state(sl, s)) return 1;
+      for (int c = 0; c < 3; ++c) {
+        out[2 * c] = sl->hst->delta[c].x;
+        out[2 * c + 1] = sl->hst->delta[c].y;
+      }
+      return 0;
+    }
+    default:
+      g_err = "slab: bad phase";
+      return 2;
+  }
+}
+
+int fftc_slab_set_delta(fftc_slab* sl, const double* delta6, void* stream) {
+  g_err.clear();
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(sl->tot_dev, delta6, sizeof(double) * 6, cudaMemcpyHostToDevice, s));
+  const double* dp = sl->tot_dev;
+  void* args[] = {&sl->row, &dp};
+  CK(cudaLaunchKernel((const void*)k_dist_set_delta, dim3(1), dim3(32), args, 0, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fftc_slab_monitor(fftc_slab* sl, const double* totals8, double* rec, void* stream) {
+  g_err.clear();
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(sl->tot_dev, totals8, sizeof(double) * 8, cudaMemcpyHostToDevice, s));
+  const double* tp = sl->tot_dev;
+  void* args[] = {&sl->row, &tp};
+  CK(cudaLaunchKernel((const void*)k_dist_monitor, dim3(1), dim3(32), args, 0, s));
+  if (slab_read_state(sl, s)) return 1;
+  DevState* h = sl->hst;
+  rec[0] = h->stopped;
+  rec[1] = h->status;
+  rec[2] = h->degenerate;
+  rec[3] = h->nrec;
+  rec[4] = h->last_sstar.x;
+  rec[5] = h->last_sstar.y;
+  rec[6] = 0.0;
+  if (h->nrec > 0) {
+    double r3[3];
+    const long long slot = (h->nrec - 1) % sl->row.hist_cap;
+    CK(cudaMemcpy(r3, sl->row.history + 3 * slot, sizeof(r3), cudaMemcpyDeviceToHost));
+    rec[4] = r3[0];
+    rec[5] = r3[1];
+    rec[6] = r3[2];
+  }
+  return 0;
+}
+
+int fftc_slab_finalize(fftc_slab* sl, void* E, void* J, void* aug, double* means12, void* stream) {
+  g_err.clear();
+  Registry& R = reg();
+  cudaStream_t s = (cudaStream_t)stream;
+  Launcher Lc(s, R.num_sms);
+  Args a = sl->row;
+  a.outE = (double2*)E;
+  a.outJ = (double2*)J;
+  a.outAug = (double2*)aug;
+  int rc;
+  switch (sl->scheme) {
+    case FFTC_BASIC: rc = launch_elementwise(k_finalize<BASIC>, Lc, (long long)a.d * a.N, a, K_FINAL); break;
+    case FFTC_EM: rc = launch_elementwise(k_finalize<EM>, Lc, (long long)a.d * a.N, a, K_FINAL); break;
+    case FFTC_BASIC_SUB: rc = launch_elementwise(k_finalize<BASIC_SUB>, Lc, (long long)a.d * a.N, a, K_FINAL); break;
+    default: rc = launch_elementwise(k_finalize<EM_SUB>, Lc, (long long)a.d * a.N, a, K_FINAL); break;
+  }
+  if (rc) return rc;
+  if (slab_read_state(sl, s)) return 1;
+  for (int c = 0; c < 3; ++c) {
+    means12[2 * c] = sl->hst->meanE[c].x;
+    means12[2 * c + 1] = sl->hst->meanE[c].y;
+    means12[6 + 2 * c] = sl->hst->meanJ[c].x;
+    means12[6 + 2 * c + 1] = sl->hst->meanJ[c].y;
+  }
+  return 0;
+}
+
+void fftc_slab_destroy(fftc_slab* sl) {
+  if (!sl) return;
+  cudaDeviceSynchronize();
+  if (sl->ws) cudaFree(sl->ws);
+  if (sl->hst) cudaFreeHost(sl->hst);
+  delete sl;
 }
 
 int fftc_solve_host(const fftc_problem* pb, const fftc_params* pr, double* history, int64_t history_cap,

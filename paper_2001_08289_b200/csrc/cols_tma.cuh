@@ -189,8 +189,10 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
   }
   if (ht == 0) bulk_wait0();  // this half's TMA stores have landed in global memory
   double tot[NQ];
-  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
-    monitor_step(a, tot[0] * (double)a.N + a.st->js2);
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode) {
+    if (a.dist) a.st->parseval = tot[0] / a.inv_n;
+    else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
+  }
 }
 
 }  // namespace fftc

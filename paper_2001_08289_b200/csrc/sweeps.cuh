@@ -77,6 +77,7 @@ struct Args {
   int op_mode;  // 1: operator API call -- no stop flag, no monitor
   DevState* st;
   unsigned long long* dbg;  // debug phase counters (FFTC_PHASE_TIMING builds), else null
+  int dist;                 // slab-decomposed solve: sweeps leave rank-local partials, the host combines
   const double2* tw[3];  // twiddles for n_x, n_y, n_z
   // scalars (host-prepared, see abi.cu)
   double2 sigma1, s0, e0[3];
@@ -543,6 +544,8 @@ struct ColGeom {
   long long stride;   // element stride along the line
   long long ostride;  // stride of the outer index
   int nstrips;        // nx / W
+  int o0;             // global index of outer = 0 (y offset of a y-slab, 3-D z pass)
+  int on;             // global extent of the outer axis (ny)
   int pad;
 };
 
@@ -604,7 +607,7 @@ __global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
         // remaining axis (3-D) from the outer index.
         const double kx = (double)wavenum(x, a.nx);
         double kyo = 0.0;
-        if constexpr (C == 3) kyo = (double)wavenum(outer, a.ny);
+        if constexpr (C == 3) kyo = (double)wavenum(gm.o0 + outer, gm.on);
         const bool parseval_only = (MODE == MID_EM) && f == 1;
 #pragma unroll
         for (int i = 0; i < E; ++i) {
@@ -656,8 +659,10 @@ __global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
   }
   if constexpr (MODE == MID_BASIC || MODE == MID_EM) {
     double tot[NQ];
-    if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
-      monitor_step(a, tot[0] * (double)a.N + a.st->js2);
+    if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode) {
+      if (a.dist) a.st->parseval = tot[0] / a.inv_n;  // rank-local sum_x |g|^2
+      else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
+    }
   }
 }
 
@@ -745,8 +750,10 @@ __global__ void __launch_bounds__(4 * (L / E)) k_mid2(Args a, ColGeom gm) {
     for (int i = 0; i < E; ++i) F[(size_t)pos_last<L, E>(true, t, i) * a.nx] = v[0][i];
   }
   double tot[NQ];
-  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode)
-    monitor_step(a, tot[0] * (double)a.N + a.st->js2);
+  if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0 && !a.op_mode) {
+    if (a.dist) a.st->parseval = tot[0] / a.inv_n;
+    else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
+  }
 }
 
 // ============================================================================

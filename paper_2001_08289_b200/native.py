@@ -26,6 +26,12 @@ EXPORTS = (
     "fftc_profile",
     "fftc_kernel_stats",
     "fftc_solve_batch",
+    "fftc_slab_create",
+    "fftc_slab_phase",
+    "fftc_slab_set_delta",
+    "fftc_slab_monitor",
+    "fftc_slab_finalize",
+    "fftc_slab_destroy",
 )
 
 FFTC_CONVERGED, FFTC_MAX_ITERS, FFTC_DIVERGED = 0, 1, 2
@@ -49,6 +55,11 @@ class Result(C.Structure):
                 ("sigma_star", C.c_double * 2), ("mean_E", (C.c_double * 2) * 3),
                 ("mean_J", (C.c_double * 2) * 3), ("kernel_launches", C.c_int64),
                 ("device_ms", C.c_double)]
+
+
+class SlabDesc(C.Structure):
+    _fields_ = [("d", C.c_int32), ("reserved", C.c_int32), ("n", C.c_int64 * 3), ("z0", C.c_int64),
+                ("nzl", C.c_int64), ("y0", C.c_int64), ("nyl", C.c_int64), ("chi", C.c_void_p)]
 
 
 class KStat(C.Structure):
@@ -82,6 +93,19 @@ def lib():
         L.fftc_solve_batch.argtypes = [C.POINTER(Problem), C.POINTER(Params), C.c_int32, vp, i64,
                                        C.POINTER(Result), vp]
         L.fftc_solve_batch.restype = C.c_int
+        L.fftc_slab_create.argtypes = [C.POINTER(SlabDesc), C.POINTER(Params), vp, vp, vp, vp,
+                                       C.POINTER(C.c_void_p), vp]
+        L.fftc_slab_create.restype = C.c_int
+        L.fftc_slab_phase.argtypes = [vp, C.c_int32, vp, vp]
+        L.fftc_slab_phase.restype = C.c_int
+        L.fftc_slab_set_delta.argtypes = [vp, vp, vp]
+        L.fftc_slab_set_delta.restype = C.c_int
+        L.fftc_slab_monitor.argtypes = [vp, vp, vp, vp]
+        L.fftc_slab_monitor.restype = C.c_int
+        L.fftc_slab_finalize.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.fftc_slab_finalize.restype = C.c_int
+        L.fftc_slab_destroy.argtypes = [vp]
+        L.fftc_slab_destroy.restype = None
         L.fftc_fft.argtypes = [C.POINTER(Problem), vp, C.c_int32, C.c_int32, vp]
         L.fftc_fft.restype = C.c_int
         L.fftc_gamma1.argtypes = [C.POINTER(Problem), vp, vp, C.c_double, vp]

@@ -1,0 +1,202 @@
+"""z-slab decomposed 3-D solve over the ranks of a process group (BASELINE
+config 4: 1024^3 random medium, "slab-decomposed across 1/2/4/8 B200 with
+NCCL all-to-all FFT transposes").
+
+Rank r owns z-planes [r*nz/G, (r+1)*nz/G) of every field.  Per iteration
+(reference loop solvers.py:300-321 / :395-432):
+
+  ROWS_FWD   local: prologue, x-FFT, y-FFT            -> partial <j>, sum|Js|^2
+  transpose  all-to-all z-slabs -> y-slabs (A, and B for EM-type schemes)
+  MID        local: z-FFT, Gamma projection, Parseval, z-iFFT -> partial residual
+  transpose  all-to-all y-slabs -> z-slabs (A)
+  all-reduce {<j>, sum|Js|^2, residual}; monitor (identical on every rank)
+  ROWS_INV   local: y-iFFT, x-iFFT, state update       -> partial <raw iterate>
+  all-reduce -> delta (mean-field pin) installed on every rank
+
+The collectives are torch.distributed all_to_all_single / all_reduce (NCCL
+over NVLink on GPUs, gloo for the CPU test).  Kernels are the same fused
+sweeps as the single-GPU path (fftc_slab_* in include/fftcond_b200.h).
+The per-rank work is a `backend` object so the decomposition logic can be
+tested on CPU with a numpy backend (tests/slab_numpy.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import native
+from .exceptions import BackendError
+from .solver import SolverConfig, TerminationStatus, _params
+
+PH_INIT, PH_ROWS_FWD, PH_MID, PH_ROWS_INV = 0, 1, 2, 3
+
+
+def _dist(group):
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist, dist.get_rank(group), dist.get_world_size(group)
+    return None, 0, 1
+
+
+def slab_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    if n % world:
+        raise ValueError(f"axis of length {n} does not split over {world} ranks")
+    m = n // world
+    return rank * m, m
+
+
+class GpuSlab:
+    """Per-rank device state behind fftc_slab_* (one rank per GPU)."""
+
+    def __init__(self, chi_local: np.ndarray, n_global, z0, nzl, y0, nyl, cfg: SolverConfig):
+        import torch
+
+        nz, ny, nx = n_global
+        self.torch = torch
+        self.em_type = cfg.scheme.accelerated
+        self.chi = torch.from_numpy(np.ascontiguousarray(chi_local).astype(np.uint8)).cuda()
+        shape_z, shape_y = (3, nzl, ny, nx), (3, nyl, nz, nx)
+        self.Az = torch.empty(shape_z, dtype=torch.complex128, device="cuda")
+        self.Ay = torch.empty(shape_y, dtype=torch.complex128, device="cuda")
+        self.Bz = torch.empty(shape_z, dtype=torch.complex128, device="cuda") if self.em_type else self.Az
+        self.By = torch.empty(shape_y, dtype=torch.complex128, device="cuda") if self.em_type else self.Ay
+        d = native.SlabDesc()
+        d.d = 3
+        d.n[0], d.n[1], d.n[2] = nx, ny, nz
+        d.z0, d.nzl, d.y0, d.nyl = z0, nzl, y0, nyl
+        d.chi = self.chi.data_ptr()
+        self.params = _params(cfg, 3)
+        self.h = C.c_void_p()
+        self.L = native.lib()
+        rc = self.L.fftc_slab_create(C.byref(d), C.byref(self.params), self.Az.data_ptr(), self.Bz.data_ptr(),
+                                     self.Ay.data_ptr(), self.By.data_ptr(), C.byref(self.h), self._stream())
+        if rc:
+            raise BackendError(f"fftc_slab_create failed ({rc}): {native.last_error()}")
+
+    def _stream(self):
+        return self.torch.cuda.current_stream().cuda_stream
+
+    def _call(self, fn, *args):
+        rc = fn(self.h, *args, self._stream())
+        if rc:
+            raise BackendError(f"{fn.__name__} failed ({rc}): {native.last_error()}")
+
+    def phase(self, ph: int) -> np.ndarray:
+        out = np.zeros(8)
+        self._call(self.L.fftc_slab_phase, ph, out.ctypes.data)
+        return out
+
+    def set_delta(self, delta6: np.ndarray):
+        d = np.ascontiguousarray(delta6, dtype=np.float64)
+        self._call(self.L.fftc_slab_set_delta, d.ctypes.data)
+
+    def monitor(self, totals8: np.ndarray) -> np.ndarray:
+        t = np.ascontiguousarray(totals8, dtype=np.float64)
+        rec = np.zeros(7)
+        self._call(self.L.fftc_slab_monitor, t.ctypes.data, rec.ctypes.data)
+        return rec
+
+    def finalize(self) -> np.ndarray:
+        m = np.zeros(12)
+        self._call(self.L.fftc_slab_finalize, None, None, None, m.ctypes.data)
+        return m
+
+    def close(self):
+        if self.h:
+            self.L.fftc_slab_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def _transpose_z_to_y(Az, Ay, world, group, dist):
+    """(c, z_l, y, x) z-slabs -> (c, y_l, z, x) y-slabs through one all-to-all."""
+    import torch
+
+    d, nzl, ny, nx = Az.shape
+    nyl = ny // world
+    send = Az.view(d, nzl, world, nyl, nx).permute(2, 0, 1, 3, 4).contiguous()
+    if world == 1:
+        recv = send
+    else:
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), group=group)
+    # recv[q] = rank q's z-planes of my y-planes: (q, c, z_l, y_l, x)
+    Ay.view(d, nyl, world, nzl, nx).copy_(recv.permute(1, 3, 0, 2, 4))
+
+
+def _transpose_y_to_z(Ay, Az, world, group, dist):
+    import torch
+
+    d, nyl, nz, nx = Ay.shape
+    nzl = nz // world
+    send = Ay.view(d, nyl, world, nzl, nx).permute(2, 0, 3, 1, 4).contiguous()  # (q, c, z_l(q), y_l, x)
+    if world == 1:
+        recv = send
+    else:
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), group=group)
+    # recv[q] = rank q's y-planes of my z-planes: (q, c, z_l, y_l, x)
+    Az.view(d, nzl, world, nyl, nx).copy_(recv.permute(1, 2, 0, 3, 4))
+
+
+def _allreduce(vec: np.ndarray, dist, group, device) -> np.ndarray:
+    if dist is None:
+        return vec
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64)).to(device)
+    dist.all_reduce(t, group=group)
+    return t.cpu().numpy()
+
+
+_STATUS = {0: TerminationStatus.CONVERGED, 1: TerminationStatus.MAX_ITERS, 2: TerminationStatus.DIVERGED}
+
+
+def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend_factory=None) -> dict:
+    """Slab-decomposed solve of a 3-D cell; every rank returns the same record dict."""
+    dist, rank, world = _dist(group)
+    chi_global = np.asarray(chi_global, dtype=bool)
+    if chi_global.ndim != 3:
+        raise ValueError("slab decomposition is for 3-D cells")
+    nz, ny, nx = chi_global.shape
+    z0, nzl = slab_bounds(nz, rank, world)
+    y0, nyl = slab_bounds(ny, rank, world)
+    factory = backend_factory or GpuSlab
+    be = factory(chi_global[z0:z0 + nzl], (nz, ny, nx), z0, nzl, y0, nyl, cfg)
+    device = "cuda" if factory is GpuSlab else "cpu"
+    e0 = cfg.e0_vector(3)
+    e0v = np.array([[z.real, z.imag] for z in e0]).ravel()
+    try:
+        def global_delta(parts):
+            tot = _allreduce(parts[:6], dist, group, device)
+            return tot - (world - 1) * e0v
+
+        be.set_delta(global_delta(be.phase(PH_INIT)))
+        history, rec = [], None
+        for k in range(1, cfg.max_iters + 1):
+            fwd = be.phase(PH_ROWS_FWD)
+            _transpose_z_to_y(be.Az, be.Ay, world, group, dist)
+            if be.em_type:
+                _transpose_z_to_y(be.Bz, be.By, world, group, dist)
+            mid = be.phase(PH_MID)
+            _transpose_y_to_z(be.Ay, be.Az, world, group, dist)
+            tot = _allreduce(np.concatenate([fwd[:7], mid[:1]]), dist, group, device)
+            rec = be.monitor(tot)
+            if int(rec[3]) > len(history):
+                history.append((complex(rec[4], rec[5]), float(rec[6])))
+            if rec[0]:
+                break
+            be.set_delta(global_delta(be.phase(PH_ROWS_INV)))
+        means = _allreduce(be.finalize(), dist, group, device)
+        sstar = history[-1][0] if history else complex(rec[4], rec[5])
+        return dict(status=_STATUS[int(rec[1])], degenerate_flux=bool(rec[2]), iterations=len(history),
+                    sigma_star=sstar, history=history,
+                    mean_E=np.array([complex(means[2 * c], means[2 * c + 1]) for c in range(3)]),
+                    mean_J=np.array([complex(means[6 + 2 * c], means[6 + 2 * c + 1]) for c in range(3)]),
+                    world=world)
+    finally:
+        close = getattr(be, "close", None)
+        if close:
+            close()
