@@ -6,6 +6,10 @@
 #include "cols_tma.cuh"
 #include "kernel_table.h"
 
+#ifndef FFTC_TMA_ROWS_MIN
+#define FFTC_TMA_ROWS_MIN 512
+#endif
+
 #ifndef FFTC_LG
 #error "define FFTC_LG before including instantiate.cuh"
 #endif
@@ -67,7 +71,7 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID2T_BASIC] = make(k_mid2_tma<MID_BASIC, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
     t.col[KC_MID2T_EM] = make(k_mid2_tma<MID_EM, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
   }
-  if constexpr (LL >= 512) {  // TMA-staged persistent row sweeps
+  if constexpr (LL >= FFTC_TMA_ROWS_MIN) {  // TMA-staged persistent row sweeps
 #define FFTC_TMA(SCH)                                                                                   \
   t.s1[SCH] = make(k_rows_tma<SCH, 1, LL>, RowTma<SCH, 1, LL>::THREADS, RowTma<SCH, 1, LL>::SMEM, 1); \
   t.s3[SCH] = make(k_rows_tma<SCH, 3, LL>, RowTma<SCH, 3, LL>::THREADS, RowTma<SCH, 3, LL>::SMEM, 1);

@@ -99,6 +99,18 @@ def test_config2_reduced(g):
     check(run_case(g["case"]), g)
 
 
+@pytest.mark.parametrize("g", _cases("c2full"))
+def test_config2_full_size(g):
+    """BASELINE configs[1] at 2048^2 against the live reference's outputs."""
+    check(run_case(g["case"]), g)
+
+
+@pytest.mark.parametrize("g", _cases("c5full"))
+def test_config5_full_size(g):
+    """BASELINE configs[4] points at 1024^2 against the live reference (complex sigma1)."""
+    check(run_case(g["case"]), g)
+
+
 @pytest.mark.parametrize("g", _cases("3d"))
 def test_3d(g):
     r = run_case(g["case"])
