@@ -28,7 +28,9 @@ struct ColTma {
   static constexpr int NSLOT = 3;
   static constexpr int CB = LP + 8;         // exchange buffer stride per component
   static constexpr int SLOT = 2 * CB + 8;   // double2 units: two skewed exchange buffers (>= 2L TMA landing)
-  static constexpr int SMEM = NSLOT * SLOT * (int)sizeof(double2);
+  // + twiddle copy: load_twbase only reads indices (R/2)*m < L/2 (m < L/R)
+  static constexpr int SMEM = (NSLOT * SLOT + L / 2) * (int)sizeof(double2);
+  static_assert(SMEM <= 232448 - 64, "column kernel exceeds the 227 KB dynamic shared memory limit");
   static constexpr int BOXR = L < 256 ? L : 256;  // rows per TMA box
   static constexpr unsigned TX = (unsigned)(2 * L * sizeof(double2));
 };
@@ -95,7 +97,14 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
   constexpr int E = K::E;
   constexpr int NQ = 1;
   extern __shared__ __align__(128) double2 smem[];
-  __shared__ uint64_t bars[K::NSLOT];
+  // bars: slot s holds line k's data (TMA complete_tx).  cbars: the half that
+  // consumed line k has released slot s.  The two halves take lines k = half,
+  // half+2, ... and share the NSLOT-ring, so line k reuses the slot of line
+  // k-NSLOT, consumed by the other half.  A half may run ahead (the EM scheme's
+  // parseval-only lines skip the inverse FFT and the store); without cbars its
+  // parity wait for line k could alias line k-2*NSLOT's completed phase while
+  // line k-NSLOT's copy is still in flight.
+  __shared__ uint64_t bars[K::NSLOT], cbars[K::NSLOT];
   if (!a.op_mode && a.st->stopped) return;
   const int half = threadIdx.x / K::HALF, ht = threadIdx.x % K::HALF;
   const int comp = ht & 1, t = ht >> 1;
@@ -104,7 +113,10 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
   const long long lines = (long long)a.nx * nfields;
   const long long nmine = blockIdx.x < lines ? (lines - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < K::NSLOT; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < K::NSLOT; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&cbars[s], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -114,6 +126,10 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
       const int f = (int)(line / a.nx);
       cols_tma_issue<L>(f == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], (int)(line - (long long)f * a.nx));
     }
+  double2* tws = smem + K::NSLOT * K::SLOT;
+  for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[i] = __ldg(&a.tw[1][i]);
+  __syncthreads();
+  const SmemTw twy{tws};
   double acc[NQ] = {0.0};
 #ifdef FFTC_PHASE_TIMING
   long long tph_ = clock64();
@@ -129,6 +145,8 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
     // (64 B) so that partner lanes hit disjoint bank groups
     double2* xbuf = slot + comp * (K::CB + 4);
     PHASE_MARK(0);
+    static_assert(K::NSLOT % 2 == 1, "line k-NSLOT must belong to the other half");
+    if (k >= K::NSLOT) mbar_wait(&cbars[s], (unsigned)((k / K::NSLOT - 1) & 1));
     mbar_wait(&bars[s], (unsigned)((k / K::NSLOT) & 1));
     PHASE_MARK(1);
     double2 v[1][E];
@@ -136,7 +154,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
     for (int i = 0; i < E; ++i) v[0][i] = inb[pos_first<L, E>(false, t, i)];
     hsync();  // slot becomes exchange scratch
     PHASE_MARK(2);
-    fft_line<L, E, 1, false>(v, t, a.tw[1], SmemBuf{xbuf, 0}, hsync);
+    fft_line<L, E, 1, false>(v, t, twy, SmemBuf{xbuf, 0}, hsync);
     PHASE_MARK(3);
     const double kx = (double)wavenum(x, a.nx);
     const bool parseval_only = (MODE == MID_EM) && f == 1;
@@ -162,7 +180,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
     }
     PHASE_MARK(4);
     if (!parseval_only) {
-      fft_line<L, E, 1, true>(v, t, a.tw[1], SmemBuf{xbuf, 0}, hsync);
+      fft_line<L, E, 1, true>(v, t, twy, SmemBuf{xbuf, 0}, hsync);
       PHASE_MARK(5);
       // outputs -> slot in the tensor layout, then one TMA store per line
       double2* outb = slot + comp * L;
@@ -178,8 +196,8 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
       hsync();  // slot s consumed
     }
     PHASE_MARK(6);
+    if (ht == 0) mbar_arrive(&cbars[s]);  // after the hsync above: every thread of this half is done with slot s
     if (ht == 0 && k + K::NSLOT < nmine) {
-      PHASE_MARK(6);
       fence_proxy_async();
       const long long nl = line + (long long)K::NSLOT * gridDim.x;
       const int nf = (int)(nl / a.nx);

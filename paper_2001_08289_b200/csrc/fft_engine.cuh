@@ -212,13 +212,24 @@ struct TwBase {
   double2 w1, w2, w4, w8;
 };
 
-template <int R>
-__device__ __forceinline__ TwBase load_twbase(const double2* __restrict__ tw, int m) {
+// Twiddle tables: global (read-only path) or a shared-memory copy.
+__device__ __forceinline__ double2 ld_tw(const double2* __restrict__ tw, int m) { return __ldg(&tw[m]); }
+struct SmemTw {
+  const double2* p;
+};
+__device__ __forceinline__ double2 ld_tw(SmemTw tw, int m) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(tw.p + m)));
+  return v;
+}
+
+template <int R, class TW>
+__device__ __forceinline__ TwBase load_twbase(TW tw, int m) {
   TwBase b;
-  b.w1 = __ldg(&tw[m]);
-  if constexpr (R >= 4) b.w2 = __ldg(&tw[2 * m]);
-  if constexpr (R >= 8) b.w4 = __ldg(&tw[4 * m]);
-  if constexpr (R >= 16) b.w8 = __ldg(&tw[8 * m]);
+  b.w1 = ld_tw(tw, m);
+  if constexpr (R >= 4) b.w2 = ld_tw(tw, 2 * m);
+  if constexpr (R >= 8) b.w4 = ld_tw(tw, 4 * m);
+  if constexpr (R >= 16) b.w8 = ld_tw(tw, 8 * m);
   return b;
 }
 
@@ -270,7 +281,8 @@ struct StageTw {
   static constexpr int Ns = P::ns(INV, S);
   static constexpr int NB = (Ns > 1) ? E / R : 1;
   TwBase b[NB];
-  __device__ __forceinline__ void load(int t, const double2* __restrict__ tw) {
+  template <class TW>
+  __device__ __forceinline__ void load(int t, TW tw) {
     if constexpr (Ns > 1) {
 #pragma unroll
       for (int k = 0; k < NB; ++k) {
@@ -353,8 +365,8 @@ __device__ __forceinline__ void stage_exchange(double2 (&v)[C][E], int t, Buf bu
   bar();
 }
 
-template <int L, int E, int C, bool INV, int S, class Buf, class Bar>
-__device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, const double2* __restrict__ tw, Buf buf, Bar bar,
+template <int L, int E, int C, bool INV, int S, class Buf, class Bar, class TW>
+__device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, TW tw, Buf buf, Bar bar,
                                          const StageTw<L, E, INV, S>& tws) {
   using P = Plan<L, E>;
   stage_compute<L, E, C, INV, S>(v, tws);
@@ -368,8 +380,8 @@ __device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, const double
 
 // Full length-L transform of C channels.  Input: element i of thread t sits
 // at pos_first(INV,t,i); output: element i at pos_last(INV,t,i).
-template <int L, int E, int C, bool INV, class Buf, class Bar>
-__device__ __forceinline__ void fft_line(double2 (&v)[C][E], int t, const double2* __restrict__ tw, Buf buf, Bar bar) {
+template <int L, int E, int C, bool INV, class Buf, class Bar, class TW>
+__device__ __forceinline__ void fft_line(double2 (&v)[C][E], int t, TW tw, Buf buf, Bar bar) {
   StageTw<L, E, INV, 0> first;  // stage 0 has Ns = 1: no twiddles
   run_from<L, E, C, INV, 0>(v, t, tw, buf, bar, first);
 }
@@ -385,6 +397,9 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

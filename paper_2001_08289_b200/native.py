@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfftcond_b200.so")
+LIB_PATH = os.environ.get("FFTC_LIB") or os.path.join(HERE, "libfftcond_b200.so")  # FFTC_LIB: A/B builds
 
 # every symbol declared in include/fftcond_b200.h
 EXPORTS = (

@@ -135,3 +135,16 @@ def test_bit_identical_histories():
     assert len(r1.history) == len(r2.history)
     for a, b in zip(r1.history, r2.history):
         assert a.sigma_star == b.sigma_star and a.residual == b.residual
+
+
+def test_repeat_determinism_long_em_sub():
+    """Repeats of a 1000-iteration em_sub solve at 1024^2 are bit identical.
+    Guards the column sweep's shared TMA ring: a half running ahead on
+    parseval-only lines once read a slot still in flight, corrupting one
+    residual record in a few hundred repeats (cols_tma.cuh, cbars)."""
+    g = load_group("c5full")["c5_1024_p004"]
+    runs = [run_case(g["case"]) for _ in range(6)]
+    h0 = [(h.sigma_star, h.residual) for h in runs[0].history]
+    assert len(h0) == 1000
+    for r in runs[1:]:
+        assert [(h.sigma_star, h.residual) for h in r.history] == h0
