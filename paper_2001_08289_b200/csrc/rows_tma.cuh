@@ -75,14 +75,19 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
   bulk_g2s(stage + K::CHI_OFF, a.chi + (size_t)row * L, (unsigned)L, bar);
 }
 
-// L2 prefetch of the phase-1 extent of the S/T (and em_sub sweep-3 Q) rows
 template <int S, int SW, int L>
-__device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, long long line, long long lines, long long rows) {
-  if (!(S == BASIC_SUB || S == EM_SUB) || line >= lines) return;
-  if (RowTma<S, SW, L>::ST_ROWS > 0) return;  // staged by TMA instead
-  const int c = (int)(line / rows);
-  const long long row = line - (long long)c * rows;
-  const int2 ext = a.row_ext[row];
+constexpr bool rows_prefetch_slots() {
+  return (S == BASIC_SUB || S == EM_SUB) && RowTma<S, SW, L>::ST_ROWS == 0;
+}
+
+// L2 prefetch of the phase-1 extent of the S/T (and em_sub sweep-3 Q) rows;
+// `ext` (that line's row_ext entry) was loaded one line earlier so the
+// prefetching warp never waits on it in front of the block barrier
+template <int S, int SW, int L>
+__device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, int line, int lines, int rows, int2 ext) {
+  if (!rows_prefetch_slots<S, SW, L>() || line >= lines) return;
+  const int c = line / rows;
+  const int row = line - c * rows;
   if (ext.x >= ext.y) return;
   const size_t off = (size_t)c * a.N + (size_t)row * L + (ext.x & ~1);
   const unsigned nb = (unsigned)((ext.y - (ext.x & ~1)) * sizeof(double2) + 15) & ~15u;
@@ -99,16 +104,24 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
   constexpr bool INV = (SW == 3);
   extern __shared__ __align__(128) double2 smem[];
   __shared__ uint64_t bars[K::NSTAGE];
+  __shared__ double2 sdelta[3];
   if (a.st->stopped) return;
   const int t = threadIdx.x % T, ch = threadIdx.x / T;
   const bool jchan = (ch == CH - 1);
-  const long long rows = (long long)a.ny * a.nz;
-  const long long lines = rows * a.d;
-  const long long nmine = blockIdx.x < lines ? (lines - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // 32-bit line bookkeeping (axes <= 4096, so rows * d <= 3 * 2^24): keeps the
+  // loop state in registers instead of local memory
+  const int rows = a.ny * a.nz;
+  const int lines = rows * a.d;
+  const int nmine = (int)blockIdx.x < lines ? (lines - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < K::NSTAGE; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
+  if (threadIdx.x < 3) sdelta[threadIdx.x] = a.st->delta[threadIdx.x];
+  // phase-1 extent of the line after next, for the S/T prefetch
+  const bool pf = rows_prefetch_slots<S, SW, L>() && threadIdx.x == blockDim.x - 1;
+  int2 ext_next = make_int2(0, 0);
+  if (pf && (int)blockIdx.x + (int)gridDim.x < lines) ext_next = a.row_ext[((int)blockIdx.x + (int)gridDim.x) % rows];
   __syncthreads();
   if (threadIdx.x == 0)
     for (int s = 0; s < K::NSTAGE && s < nmine; ++s)
@@ -118,17 +131,22 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
   double2* xbuf = smem + K::NSTAGE * K::STAGE;
   double2* OUT = (SW == 1 && CH == 2 && ch == 1) ? a.B : a.A;
-  for (long long k = 0; k < nmine; ++k) {
-    const int s = (int)(k % K::NSTAGE);
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k % K::NSTAGE;
     const unsigned parity = (unsigned)((k / K::NSTAGE) & 1);
-    const long long line = blockIdx.x + k * gridDim.x;
-    const int c = (int)(line / rows);
-    const long long row = line - (long long)c * rows;
+    const int line = (int)blockIdx.x + k * (int)gridDim.x;
+    const int c = line / rows;
+    const int row = line - c * rows;
     const size_t off = (size_t)c * a.N + (size_t)row * L;
-    const double2 dl = a.st->delta[c];
+    const double2 dl = sdelta[c];
     double2* st = smem + s * K::STAGE;
     const uint8_t* chi_s = reinterpret_cast<const uint8_t*>(st + K::CHI_OFF);
-    if (threadIdx.x == blockDim.x - 1) rows_tma_prefetch_slots<S, SW, L>(a, line + gridDim.x, lines, rows);
+    if (pf) {
+      const int2 ext = ext_next;
+      const int l2 = line + 2 * (int)gridDim.x;
+      if (l2 < lines) ext_next = a.row_ext[l2 % rows];
+      rows_tma_prefetch_slots<S, SW, L>(a, line + (int)gridDim.x, lines, rows, ext);
+    }
     mbar_wait(&bars[s], parity);
     double2 v[1][E];
     if constexpr (SW == 1) {
@@ -231,7 +249,7 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
     __syncthreads();  // stage s fully consumed (exchange, chi, X0 row)
     if (threadIdx.x == 0 && k + K::NSTAGE < nmine) {
       fence_proxy_async();
-      rows_tma_issue<S, SW, L>(a, st, &bars[s], line + (long long)K::NSTAGE * gridDim.x, rows);
+      rows_tma_issue<S, SW, L>(a, st, &bars[s], (long long)line + (long long)K::NSTAGE * gridDim.x, rows);
     }
   }
   double tot[NQ];
