@@ -144,6 +144,37 @@ int fftc_solve_host(const fftc_problem* problem_with_host_chi, const fftc_params
 int fftc_fft(const fftc_problem* problem, void* data, int32_t inverse, int32_t axes_mask, void* stream);
 int fftc_gamma1(const fftc_problem* problem, const void* in, void* out, double scale, void* stream);
 
+/* Pointwise augmented-space operators on DEVICE (Q, S, T) fields, each
+ * d*N complex128 (AugmentedField, spectral_ops.py:141-173), chi from the
+ * problem.  coef = {p1, p2, p3, t, sigma0} as (re, im) pairs (10 doubles).
+ *   FFTC_AUG_CHI         apply_chi_aug     (spectral_ops.py:227-237): (p1 u, p2 u, p3 u),
+ *                        u = chi (p1 Q + p2 S + p3 T)
+ *   FFTC_AUG_LOCAL_A     apply_local_A     (spectral_ops.py:240-250): A = (t-1) chi'' + I
+ *   FFTC_AUG_INV_SHIFTED invert_shifted_A  (spectral_ops.py:253-278): (A + sigma0 I)^-1
+ * S and T outputs are zero off chi.  Outputs may alias inputs.  The
+ * singular-shift checks (sigma0 = -1, sigma0 = -t) are the host layer's. */
+enum { FFTC_AUG_CHI = 0, FFTC_AUG_LOCAL_A = 1, FFTC_AUG_INV_SHIFTED = 2 };
+int fftc_aug_apply(const fftc_problem* problem, int32_t op, const double* coef, const void* Q, const void* S,
+                   const void* T, void* Q_out, void* S_out, void* T_out, void* stream);
+
+/* j = sigma e on DEVICE fields, sigma = sigma1 on chi and 1 elsewhere
+ * (extract_sigma_star, solvers.py:147-155; the loop's j, :286, :311). */
+int fftc_apply_sigma(const fftc_problem* problem, const double* sigma1, const void* e, void* j, void* stream);
+
+/* Deterministic reductions of DEVICE fields (fixed-order trees; the
+ * reference's compensated sums, spectral_ops.py:33-55, :96-106, :182-200).
+ * Results go to the HOST array out; the call synchronises the stream.
+ *   FFTC_RED_SUM          out[2d]: per-component sums of a (re, im)
+ *   FFTC_RED_DOT          out[2]:  sum over components and voxels of conj(a) b
+ *   FFTC_RED_NORM2        out[1]:  sum |a|^2
+ *   FFTC_RED_OFF_SUPPORT  out[1]:  number of phase-2 voxels where a (or b,
+ *                                  nullable) is nonzero (_check_support, :176-179)
+ * mask = FFTC_MASK_CHI restricts SUM/DOT/NORM2 to phase-1 voxels. */
+enum { FFTC_RED_SUM = 0, FFTC_RED_DOT = 1, FFTC_RED_NORM2 = 2, FFTC_RED_OFF_SUPPORT = 3 };
+enum { FFTC_MASK_NONE = 0, FFTC_MASK_CHI = 1 };
+int fftc_reduce(const fftc_problem* problem, int32_t op, int32_t mask, const void* a, const void* b, double* out,
+                void* stream);
+
 /* Per-kernel timing.  fftc_profile(1) resets the counters and brackets every
  * subsequent library launch with CUDA events on its stream (device time,
  * harvested at the solver's existing synchronisation points);

@@ -367,3 +367,109 @@ def centred_box(n: int, side: int, d: int = 2) -> np.ndarray:
     lo = (n - side) // 2
     chi[tuple(slice(lo, lo + side) for _ in range(d))] = True
     return chi
+
+
+# --------------------------------------------------------------------------
+# public operator surface (spectral_ops.py:96-278, solvers.py:147-204),
+# d-generic restatements on (d, *grid) arrays; aug fields are (Q, S, T)
+# tuples.  Same numpy operation order as the reference.
+# --------------------------------------------------------------------------
+
+def inner(f, g) -> complex:
+    """spectral_ops.py:96-99: mean of conj(f).g over all components."""
+    return total_complex(np.conj(f) * g) / int(np.prod(f.shape[1:]))
+
+
+def norm(f) -> float:
+    """spectral_ops.py:102-106."""
+    return math.sqrt(total_real(np.abs(f) ** 2) / int(np.prod(f.shape[1:])))
+
+
+def gamma0(f) -> np.ndarray:
+    """spectral_ops.py:136-138 (VectorField.mean)."""
+    return component_means(f)
+
+
+def inner_aug(F, G, chi) -> complex:
+    """spectral_ops.py:182-190."""
+    total = total_complex(np.conj(F[0]) * G[0])
+    total += total_complex((np.conj(F[1]) * G[1] + np.conj(F[2]) * G[2]) * chi)
+    return total / chi.size
+
+
+def norm_aug(F, chi) -> float:
+    """spectral_ops.py:193-200."""
+    total = total_real(np.abs(F[0]) ** 2)
+    total += total_real((np.abs(F[1]) ** 2 + np.abs(F[2]) ** 2) * chi)
+    return math.sqrt(total / chi.size)
+
+
+def off_support(F, chi) -> bool:
+    """spectral_ops.py:176-179: S or T nonzero on a phase-2 voxel."""
+    outside = ~chi
+    return bool(np.any(F[1][:, outside]) or np.any(F[2][:, outside]))
+
+
+def gamma1_aug(F, chi, scale: float = 1.0):
+    """spectral_ops.py:208-212: (Gamma_1 Q, S, 0); raises on off-support data."""
+    if off_support(F, chi):
+        raise ValueError("S/T slots carry data on phase-2 pixels")
+    return gamma1(F[0], scale), F[1].copy(), np.zeros_like(F[1])
+
+
+def _chi_aug(F, p, chi):
+    """spectral_ops.py:215-224."""
+    u = p[0] * F[0] + p[1] * F[1] + p[2] * F[2]
+    u = np.where(chi, u, 0.0)
+    return p[0] * u, p[1] * u, p[2] * u
+
+
+def apply_chi_aug(F, p, chi):
+    """spectral_ops.py:227-237."""
+    return _chi_aug(F, p, chi)
+
+
+def apply_local_A(F, t, p, chi):
+    """spectral_ops.py:240-250 (same algebra as apply_A, reference op order)."""
+    qo, so, to = _chi_aug(F, p, chi)
+    tm1 = complex(t) - 1.0
+    return (tm1 * qo + F[0], np.where(chi, tm1 * so + F[1], 0.0), np.where(chi, tm1 * to + F[2], 0.0))
+
+
+def invert_shifted_A(F, t, sigma0, p, chi):
+    """spectral_ops.py:253-278 (the singular-shift checks are the caller's)."""
+    tt, s0 = complex(t), complex(sigma0)
+    qo, so, to = _chi_aug(F, p, chi)
+    c = (tt - 1.0) / (tt + s0)
+    scale = 1.0 / (1.0 + s0)
+    return (scale * (F[0] - c * qo), np.where(chi, scale * (F[1] - c * so), 0.0),
+            np.where(chi, scale * (F[2] - c * to), 0.0))
+
+
+def extract_sigma_star(e, chi, sigma1, e0) -> complex:
+    """solvers.py:147-155."""
+    e0v = np.array([complex(x) for x in e0])
+    sigma = np.where(chi, complex(sigma1), 1.0 + 0j)
+    jmean = component_means(sigma * e)
+    return complex(np.vdot(e0v, jmean)) / np.vdot(e0v, e0v).real
+
+
+def extract_sigma_star_aug(F, t, p, chi, e0) -> complex:
+    """solvers.py:158-171."""
+    e0v = np.array([complex(x) for x in e0])
+    flux = apply_local_A(F, t, p, chi)
+    return complex(np.vdot(e0v, component_means(flux[0]))) / np.vdot(e0v, e0v).real
+
+
+def equilibrium_residual(j, scale: float = 1.0) -> float:
+    """solvers.py:187-192."""
+    den = float(np.linalg.norm(component_means(j)))
+    return norm(gamma1(j, scale)) / den
+
+
+def equilibrium_residual_aug(J, chi, scale: float = 1.0) -> float:
+    """solvers.py:195-204."""
+    den = float(np.linalg.norm(component_means(J[0])))
+    g = gamma1(J[0], scale)
+    total = total_real(np.abs(g) ** 2) + total_real(np.abs(J[1]) ** 2 * chi)
+    return math.sqrt(total / chi.size) / den

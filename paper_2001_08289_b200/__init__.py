@@ -27,7 +27,17 @@ from .exceptions import (
     SupportError,
 )
 from .fields import AugmentedField, VectorField
-from .scalars import SchemeKind, SpectralInterval, SubstitutionParams, map_t, map_z, solve_p
+from .scalars import (
+    SchemeKind,
+    SpectralInterval,
+    SubstitutionParams,
+    aux_constants,
+    inverse_map_t,
+    map_t,
+    map_z,
+    solve_p,
+    verify_sigma1,
+)
 from .solver import (
     ConvergenceHistory,
     HistoryRecord,
@@ -42,6 +52,25 @@ from .solver import (
     solve_em_sub,
 )
 
+from .spectral import (
+    apply_chi_aug,
+    apply_local_A,
+    equilibrium_residual,
+    equilibrium_residual_aug,
+    extract_sigma_star,
+    extract_sigma_star_aug,
+    gamma0,
+    gamma0_aug,
+    gamma1,
+    gamma1_aug,
+    inner,
+    inner_aug,
+    invert_shifted_A,
+    norm,
+    norm_aug,
+    recover_physical_fields,
+)
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -51,5 +80,8 @@ __all__ = [
     "SubstitutionParams", "SupportError", "TerminationStatus", "VectorField", "build_cube_array",
     "build_disk_array", "build_random_medium", "build_square_array", "build_uniform", "estimate_rate",
     "map_t", "map_z", "solve", "solve_basic", "solve_basic_sub", "solve_em", "solve_em_sub", "solve_p",
-    "volume_fraction",
+    "volume_fraction", "aux_constants", "inverse_map_t", "verify_sigma1", "apply_chi_aug", "apply_local_A",
+    "equilibrium_residual", "equilibrium_residual_aug", "extract_sigma_star", "extract_sigma_star_aug", "gamma0",
+    "gamma0_aug", "gamma1", "gamma1_aug", "inner", "inner_aug", "invert_shifted_A", "norm", "norm_aug",
+    "recover_physical_fields",
 ]

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/fftcond_b200.h"
+#include "host_common.h"
 #include "kernel_table.h"
 #include "sweeps.cuh"
 
@@ -1265,3 +1266,16 @@ int fftc_solve_host(const fftc_problem* pb, const fftc_params* pr, double* histo
 }
 
 }  // extern "C"
+
+namespace fftc {
+void set_last_error(const std::string& msg) { g_err = msg; }
+void clear_last_error() { g_err.clear(); }
+void add_launches(long long n) { g_launches += n; }
+int device_sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  return n;
+}
+}  // namespace fftc
+

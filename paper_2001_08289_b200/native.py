@@ -14,6 +14,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FFTC_LIB") or os.path.join(HERE, "libfftcond_b200.so")  # FFTC_LIB: A/B builds
 
 # every symbol declared in include/fftcond_b200.h
+FFTC_AUG_CHI, FFTC_AUG_LOCAL_A, FFTC_AUG_INV_SHIFTED = 0, 1, 2
+FFTC_RED_SUM, FFTC_RED_DOT, FFTC_RED_NORM2, FFTC_RED_OFF_SUPPORT = 0, 1, 2, 3
+FFTC_MASK_NONE, FFTC_MASK_CHI = 0, 1
+
 EXPORTS = (
     "fftc_solve",
     "fftc_solve_host",
@@ -23,6 +27,9 @@ EXPORTS = (
     "fftc_launch_count",
     "fftc_fft",
     "fftc_gamma1",
+    "fftc_aug_apply",
+    "fftc_apply_sigma",
+    "fftc_reduce",
     "fftc_profile",
     "fftc_kernel_stats",
     "fftc_solve_batch",
@@ -110,6 +117,12 @@ def lib():
         L.fftc_fft.restype = C.c_int
         L.fftc_gamma1.argtypes = [C.POINTER(Problem), vp, vp, C.c_double, vp]
         L.fftc_gamma1.restype = C.c_int
+        L.fftc_aug_apply.argtypes = [C.POINTER(Problem), C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.fftc_aug_apply.restype = C.c_int
+        L.fftc_apply_sigma.argtypes = [C.POINTER(Problem), vp, vp, vp, vp]
+        L.fftc_apply_sigma.restype = C.c_int
+        L.fftc_reduce.argtypes = [C.POINTER(Problem), C.c_int32, C.c_int32, vp, vp, vp, vp]
+        L.fftc_reduce.restype = C.c_int
         L.fftc_profile.argtypes = [C.c_int32]
         L.fftc_profile.restype = None
         L.fftc_kernel_stats.argtypes = [C.POINTER(KStat), C.c_int32]

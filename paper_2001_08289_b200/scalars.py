@@ -12,7 +12,7 @@ import math
 from dataclasses import dataclass
 from enum import Enum
 
-from .exceptions import BranchCutError, IntervalError, PoleError
+from .exceptions import BranchCutError, DegenerateParamError, IntervalError, PoleError
 
 _REL_TOL = 1e-12
 
@@ -112,3 +112,34 @@ def solve_p(interval: SpectralInterval) -> SubstitutionParams:
         p3 = -p3
     return SubstitutionParams(interval=interval, p1=complex(math.sqrt(sq1)),
                               p2=1j * math.sqrt(-sq2), p3=p3)
+
+
+def inverse_map_t(t: complex, interval: SpectralInterval) -> complex:
+    """Inverse of map_t (transform.py:113-122); pole at t = (1+beta)/(1+alpha)."""
+    tt = complex(t)
+    a, b = interval.alpha, interval.beta
+    den = tt * (1.0 + a) - (1.0 + b)
+    if den == 0:
+        raise PoleError(f"inverse_map_t has a pole at t = {(1.0 + b) / (1.0 + a)}")
+    return (a * (1.0 + b) - b * tt * (1.0 + a)) / den
+
+
+def _coupling_denominator(t: complex, params: SubstitutionParams) -> complex:
+    """(t-1) p2^2 + 1 (transform.py:171-177)."""
+    den = (t - 1.0) * params.p2 ** 2 + 1.0
+    if den == 0:
+        raise DegenerateParamError(f"(t-1)*p2^2 + 1 vanishes at t = {t}; coupling is degenerate")
+    return den
+
+
+def aux_constants(t: complex, params: SubstitutionParams) -> tuple[complex, complex]:
+    """(E2p, J3p): slot couplings of the gradient- and flux-type fields (transform.py:180-190)."""
+    tt = complex(t)
+    den = _coupling_denominator(tt, params)
+    return (1.0 - tt) * params.p1 * params.p2 / den, params.p1 * params.p3 * (tt - 1.0) / den
+
+
+def verify_sigma1(t: complex, params: SubstitutionParams) -> complex:
+    """sigma1 reproduced by the 3-vector model at t (transform.py:193-201)."""
+    tt = complex(t)
+    return 1.0 + params.p1 ** 2 * (tt - 1.0) / _coupling_denominator(tt, params)
