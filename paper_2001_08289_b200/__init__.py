@@ -13,6 +13,10 @@ from .cell import (
     build_random_medium,
     build_square_array,
     build_uniform,
+    load_chi_bits,
+    load_raster,
+    save_chi_bits,
+    save_raster,
     volume_fraction,
 )
 from .exceptions import (
@@ -83,5 +87,5 @@ __all__ = [
     "volume_fraction", "aux_constants", "inverse_map_t", "verify_sigma1", "apply_chi_aug", "apply_local_A",
     "equilibrium_residual", "equilibrium_residual_aug", "extract_sigma_star", "extract_sigma_star_aug", "gamma0",
     "gamma0_aug", "gamma1", "gamma1_aug", "inner", "inner_aug", "invert_shifted_A", "norm", "norm_aug",
-    "recover_physical_fields",
+    "recover_physical_fields", "load_chi_bits", "load_raster", "save_chi_bits", "save_raster",
 ]

@@ -149,3 +149,95 @@ def build_random_medium(n: int, dim: int = 3, *, seed: int, smoothing: float, fr
     s = np.fft.ifftn(np.fft.fftn(u) * np.exp(-2.0 * np.pi ** 2 * smoothing ** 2 * k2)).real
     thr = np.quantile(s, fraction)
     return PhaseMap(s <= thr)
+
+
+# -- phase-map files ---------------------------------------------------------------
+RASTER_MAGIC = "P-PHASE"  # geometry.py:17
+
+
+def save_raster(pmap: PhaseMap) -> str:
+    """2-D plain-text raster of the reference (geometry.py:126-136):
+    ``P-PHASE <nx> <ny>`` then ny rows of nx 0/1 tokens, row 0 first."""
+    if pmap.dim != 2:
+        raise ValueError("the P-PHASE text raster is 2-D; use save_chi_bits for 3-D cells")
+    lines = [f"{RASTER_MAGIC} {pmap.nx} {pmap.ny}"]
+    for row in pmap.chi:
+        lines.append(" ".join("1" if v else "0" for v in row))
+    return "\n".join(lines) + "\n"
+
+
+def load_raster(text: str) -> PhaseMap:
+    """Parse :func:`save_raster` output (geometry.py:139-189); faults raise
+    RasterParseError naming line and column, as the reference does."""
+    from .exceptions import RasterParseError
+
+    lines = text.splitlines()
+    if not lines or not lines[0].strip():
+        raise RasterParseError("missing header", line=1)
+    header = lines[0].split()
+    if header[0] != RASTER_MAGIC:
+        raise RasterParseError(f"expected magic {RASTER_MAGIC!r}", line=1, column=1)
+    if len(header) != 3:
+        raise RasterParseError(f"header needs 3 tokens, got {len(header)}", line=1, column=len(header))
+    try:
+        nx, ny = int(header[1]), int(header[2])
+    except ValueError:
+        raise RasterParseError("dimensions must be integers", line=1, column=2) from None
+    if nx < 2 or ny < 2 or nx % 2 or ny % 2:
+        raise RasterParseError(f"dims must be even and >= 2, got {nx} x {ny}", line=1, column=2)
+    chi = np.zeros((ny, nx), dtype=bool)
+    for j in range(ny):
+        lineno = j + 2
+        if j + 1 >= len(lines):
+            raise RasterParseError(f"missing data row {j}", line=lineno)
+        tokens = lines[j + 1].split()
+        if len(tokens) != nx:
+            raise RasterParseError(f"expected {nx} tokens, got {len(tokens)}", line=lineno,
+                                   column=min(len(tokens), nx) + 1)
+        for i, tok in enumerate(tokens):
+            if tok == "1":
+                chi[j, i] = True
+            elif tok != "0":
+                raise RasterParseError(f"token must be 0 or 1, got {tok!r}", line=lineno, column=i + 1)
+    for extra, line in enumerate(lines[ny + 1:], start=ny + 2):
+        if line.strip():
+            raise RasterParseError("unexpected trailing content", line=extra)
+    return PhaseMap(chi)
+
+
+# Bit-packed binary phase map (SURVEY 8(f)4): the text raster costs ~2 bytes
+# per voxel and is 2-D only; at 1024^3 this format is 128 MiB.
+#   bytes 0-7   magic b"FFTCHI01"
+#   bytes 8-11  uint32 LE d (2 or 3);  bytes 12-15 reserved (0)
+#   bytes 16-39 int64 LE nx, ny, nz (nz = 1 for d = 2)
+#   bytes 40-   chi in C order (z, y, x), 8 voxels per byte, least
+#               significant bit first (numpy packbits bitorder="little")
+CHI_BITS_MAGIC = b"FFTCHI01"
+
+
+def save_chi_bits(pmap: PhaseMap, path) -> None:
+    chi = pmap.chi
+    nz = pmap.nz
+    head = CHI_BITS_MAGIC + np.array([pmap.dim, 0], "<u4").tobytes() + np.array([pmap.nx, pmap.ny, nz], "<i8").tobytes()
+    with open(path, "wb") as fh:
+        fh.write(head)
+        fh.write(np.packbits(chi.reshape(-1), bitorder="little").tobytes())
+
+
+def load_chi_bits(path) -> PhaseMap:
+    from .exceptions import RasterParseError
+
+    with open(path, "rb") as fh:
+        head = fh.read(40)
+        if len(head) < 40 or head[:8] != CHI_BITS_MAGIC:
+            raise RasterParseError("not a bit-packed phase map (bad magic)", line=1, column=1)
+        d = int(np.frombuffer(head[8:12], "<u4")[0])
+        nx, ny, nz = (int(v) for v in np.frombuffer(head[16:40], "<i8"))
+        if d not in (2, 3) or (d == 2 and nz != 1) or min(nx, ny, nz) < 1:
+            raise RasterParseError(f"bad header: d={d}, n=({nx}, {ny}, {nz})", line=1, column=2)
+        count = nx * ny * nz
+        body = np.frombuffer(fh.read(), dtype=np.uint8)
+    if body.size != (count + 7) // 8:
+        raise RasterParseError(f"expected {(count + 7) // 8} data bytes, got {body.size}", line=1, column=3)
+    chi = np.unpackbits(body, count=count, bitorder="little").astype(bool)
+    return PhaseMap(chi.reshape((nz, ny, nx) if d == 3 else (ny, nx)))
