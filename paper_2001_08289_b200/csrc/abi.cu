@@ -16,6 +16,7 @@
 #include <cmath>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fftcond_b200.h"
@@ -947,13 +948,67 @@ int fftc_solve_batch(const fftc_problem* pb, const fftc_params* params, int32_t 
     g_err = "null argument";
     return 2;
   }
-  for (int32_t i = 0; i < n_points; ++i) {
-    int rc = fftc_solve(pb, &params[i], histories + (size_t)i * history_cap * 3, history_cap, nullptr, nullptr,
-                        nullptr, &out[i], stream);
-    if (rc) {
-      g_err = "point " + std::to_string(i) + ": " + g_err;
-      return rc;
+  // Points are independent solves.  Small and medium grids leave the GPU
+  // idle between a solve's kernels (launch tails, the per-solve setup and
+  // read-back), so several points run concurrently, one host worker and one
+  // non-blocking stream each (FFTC_BATCH_STREAMS, default 4; 1 = in order).
+  // Every solve is deterministic on its own, so the results do not depend on
+  // the interleaving.
+  int width = 4;
+  if (const char* e = getenv("FFTC_BATCH_STREAMS")) width = std::max(1, atoi(e));
+  width = std::min<int>(width, std::max<int32_t>(n_points, 1));
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (g_profile) width = 1;  // per-kernel statistics are collected in launch order
+  }
+  if (width <= 1) {
+    for (int32_t i = 0; i < n_points; ++i) {
+      int rc = fftc_solve(pb, &params[i], histories + (size_t)i * history_cap * 3, history_cap, nullptr, nullptr,
+                          nullptr, &out[i], stream);
+      if (rc) {
+        g_err = "point " + std::to_string(i) + ": " + g_err;
+        return rc;
+      }
     }
+    return 0;
+  }
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  cudaEvent_t ready;
+  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CK(cudaEventRecord(ready, (cudaStream_t)stream));  // chi and friends are ordered on the caller's stream
+  std::atomic<int32_t> next{0};
+  std::atomic<int> first_bad{-1};
+  std::vector<int> rcs(n_points, 0);
+  std::vector<std::string> errs(n_points);
+  auto worker = [&]() {
+    cudaSetDevice(dev);
+    cudaStream_t ws = nullptr;
+    if (cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking) != cudaSuccess) {
+      first_bad = 0;
+      return;
+    }
+    cudaStreamWaitEvent(ws, ready, 0);
+    for (int32_t i; first_bad.load() < 0 && (i = next.fetch_add(1)) < n_points;) {
+      rcs[i] = fftc_solve(pb, &params[i], histories + (size_t)i * history_cap * 3, history_cap, nullptr, nullptr,
+                          nullptr, &out[i], ws);
+      if (rcs[i]) {
+        errs[i] = g_err;
+        int expect = -1;
+        first_bad.compare_exchange_strong(expect, i);
+      }
+    }
+    cudaStreamSynchronize(ws);
+    cudaStreamDestroy(ws);
+  };
+  std::vector<std::thread> pool;
+  for (int w = 0; w < width; ++w) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  cudaEventDestroy(ready);
+  const int bad = first_bad.load();
+  if (bad >= 0) {
+    g_err = "point " + std::to_string(bad) + ": " + (errs[bad].empty() ? "stream setup failed" : errs[bad]);
+    return rcs[bad] ? rcs[bad] : 1;
   }
   return 0;
 }
