@@ -107,7 +107,11 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
   __shared__ uint64_t bars[K::NSLOT], cbars[K::NSLOT];
   if (!a.op_mode && a.st->stopped) return;
   const int half = threadIdx.x / K::HALF, ht = threadIdx.x % K::HALF;
-  const int comp = ht & 1, t = ht >> 1;
+  // component in lane bit CB (16 lanes of one component side by side): an
+  // 8-lane LDS.128 phase then reads 128 contiguous bytes of one component
+  // instead of two components whose [comp][y] landing rows share banks
+  constexpr int CB = K::T >= 16 ? 4 : (K::T >= 8 ? 3 : (K::T >= 4 ? 2 : (K::T >= 2 ? 1 : 0)));
+  const int comp = (ht >> CB) & 1, t = (ht & ((1 << CB) - 1)) | ((ht >> (CB + 1)) << CB);
   const HalfSync hsync{1 + half, K::HALF};
   const int nfields = (MODE == MID_EM) ? 2 : 1;
   const long long lines = (long long)a.nx * nfields;
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
       cols_tma_issue<L>(f == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], (int)(line - (long long)f * a.nx));
     }
   double2* tws = smem + K::NSLOT * K::SLOT;
-  for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[i] = __ldg(&a.tw[1][i]);
+  for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[1][i]);
   __syncthreads();
   const SmemTw twy{tws};
   double acc[NQ] = {0.0};
@@ -166,8 +170,8 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
       const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
       const double2 mine = cscale(v[0][i], kc);
       double2 other;
-      other.x = __shfl_xor_sync(0xffffffffu, mine.x, 1);
-      other.y = __shfl_xor_sync(0xffffffffu, mine.y, 1);
+      other.x = __shfl_xor_sync(0xffffffffu, mine.x, 1 << CB);
+      other.y = __shfl_xor_sync(0xffffffffu, mine.y, 1 << CB);
       double2 dot = comp ? cadd(other, mine) : cadd(mine, other);  // kx F_x + ky F_y
       dot = cscale(dot, ik2);
       if (MODE == MID_BASIC || parseval_only) {

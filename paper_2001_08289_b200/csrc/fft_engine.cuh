@@ -214,12 +214,19 @@ struct TwBase {
 
 // Twiddle tables: global (read-only path) or a shared-memory copy.
 __device__ __forceinline__ double2 ld_tw(const double2* __restrict__ tw, int m) { return __ldg(&tw[m]); }
+// Shared-memory copy of a table, swizzled so that any 8 consecutive
+// multiples of a power-of-two stride land in 8 distinct 16-byte bank groups
+// (a Stockham stage with Ns*R < L reads w^(k*L/(Ns*R)): strides 16..64 that
+// would otherwise put a whole 8-lane LDS.128 phase in one bank group).
+__host__ __device__ __forceinline__ int tw_swz(int m) { return (m & ~7) | ((m ^ (m >> 3) ^ (m >> 6) ^ (m >> 9)) & 7); }
 struct SmemTw {
-  const double2* p;
+  const double2* p;  // table stored at tw_swz(m)
 };
 __device__ __forceinline__ double2 ld_tw(SmemTw tw, int m) {
   double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"((unsigned)__cvta_generic_to_shared(tw.p + m)));
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "r"((unsigned)__cvta_generic_to_shared(tw.p + tw_swz(m))));
   return v;
 }
 
