@@ -586,6 +586,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       cudaGraphExec_t ge = nullptr;
       cudaGraphConditionalHandle h;
       cudaStream_t cs = capture_stream();
+      long long per_iter_launches = 0;
       do {
         if ((rc = (cudaGraphCreate(&g, 0) != cudaSuccess))) break;
         if ((rc = (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess))) break;
@@ -602,6 +603,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
           break;
         Launcher Lcap(cs, R.num_sms);
         int r1 = launch_iter(Lcap);
+        per_iter_launches = Lcap.count + 1;  // + the condition kernel below
         const DevState* stp = a.st;
         void* ca[] = {&h, &stp};
         if (!r1) r1 = Lcap.raw((const void*)k_loop_cond, 1, 1, 0, ca, K_OP);
@@ -627,8 +629,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
           CK(cudaMemcpy(history, a.history, sizeof(double) * 3 * nrec, cudaMemcpyDeviceToHost));
         }
         // launches executed by the loop: (kernels per body) x iterations run
-        const long long per_iter = (d == 3 ? (em_type ? 6 : 5) : 3) + 1;
-        Lc.count += per_iter * std::max<long long>(hst->k, 1);
+        Lc.count += per_iter_launches * std::max<long long>(hst->k, 1);
       }
       if (ge) cudaGraphExecDestroy(ge);
       if (g) cudaGraphDestroy(g);

@@ -9,7 +9,7 @@
 // every other line, so two lines are in compute while the third streams in.
 // A slot doubles as the line's FFT exchange buffer once its data is in
 // registers.  Per element: y-FFT (radix 16, two exchanges), the Gamma_1
-// projection with the partner component in lane^1 (spectral_ops.py:124-127),
+// projection with the partner component in lane^16 (spectral_ops.py:124-127),
 // Parseval residual accumulation, y-iFFT and a direct store.
 #pragma once
 #include <cuda.h>
@@ -186,7 +186,10 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
     if (!parseval_only) {
       fft_line<L, E, 1, true>(v, t, twy, SmemBuf{xbuf, 0}, hsync);
       PHASE_MARK(5);
-      // outputs -> slot in the tensor layout, then one TMA store per line
+      // outputs -> slot in the tensor layout, then one TMA store per line;
+      // the barrier first: another warp of this half may still be reading its
+      // last exchange from padded addresses the dense outputs overwrite
+      hsync();
       double2* outb = slot + comp * L;
 #pragma unroll
       for (int i = 0; i < E; ++i) outb[pos_last<L, E>(true, t, i)] = v[0][i];

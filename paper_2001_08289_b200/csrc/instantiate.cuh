@@ -32,15 +32,9 @@ constexpr int E_COL = L >= FFTC_E_COL ? FFTC_E_COL : L;
 constexpr int T_COL = L / E_COL;
 constexpr int W2 = L >= 4096 ? 1 : 2;
 constexpr int G2 = (T_COL * W2) >= 64 ? 1 : 64 / (T_COL * W2);
-#ifndef FFTC_W3
-#define FFTC_W3 2
-#endif
-#ifndef FFTC_WP
-#define FFTC_WP 2
-#endif
-constexpr int W3 = L >= 2048 ? 1 : (L >= 1024 && FFTC_W3 > 4 ? 4 : FFTC_W3);
+constexpr int W3 = L >= 2048 ? 1 : 2;  // k_col indexes strips assuming W <= 2
 constexpr int G3 = (T_COL * W3) >= 64 ? 1 : 64 / (T_COL * W3);
-constexpr int WP = L >= 1024 && FFTC_WP > 4 ? 4 : FFTC_WP;  // plain 3-D y passes
+constexpr int WP = 2;  // plain 3-D y passes
 constexpr int GP = (T_COL * WP) >= 64 ? 1 : 64 / (T_COL * WP);
 
 template <int C, int W, int G>
