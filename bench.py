@@ -50,6 +50,24 @@ WORKLOADS = {
 }
 
 
+def _ncu_traffic(kernel, it_by_scheme, n):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    capture (profiles/r1_ncu_traffic.json), weighted like the algorithmic
+    bytes; None when the capture does not cover this kernel/grid/schemes."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+    except OSError:
+        return None, None
+    per = t.get("kernels", {}).get(kernel, {})
+    if t.get("grid") != [n, n] or not all(s in per for s in it_by_scheme):
+        return None, None
+    tot = sum(it_by_scheme.values())
+    bytes_ = sum((per[s]["dram_read"] + per[s]["dram_write"]) * k for s, k in it_by_scheme.items()) / tot
+    return bytes_, t.get("source")
+
+
 def _peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -350,8 +368,9 @@ def run_ours(a):
         bpv = sum(_bytes_per_voxel(s, 2, frac)[name] * n for s, n in it_by_scheme.items()) / tot_it
         per_launch_ms = tms / nl
         achieved = bpv * N / (per_launch_ms / 1e3) / 1e9
+        traffic, traffic_src = _ncu_traffic(name, it_by_scheme, N_GRID)
         roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "bytes_per_launch": bpv * N, "avg_launch_ms": per_launch_ms, "launches": nl,
                 "share_of_step": tms / prof_ms if prof_ms > 0 else None,
                 "timing": "CUDA events around every launch of one profiled step (one iteration per sync)"}
