@@ -180,6 +180,54 @@ bool make_field_map(CUtensorMap* tm, void* base, long long nx, long long ny, int
   return r == CUDA_SUCCESS;
 }
 
+// 5-D map for the 3-D column passes: lines of length L at element stride
+// line_stride, nouter of them at outer_stride, three components at
+// comp_stride; a box is W adjacent x-columns of all three components
+// {2W doubles, 256 rows, L/256 blocks, 1, 3} (cols3_tma.cuh).
+bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W, long long line_stride,
+                   long long nouter, long long outer_stride, long long comp_stride) {
+  EncodeTiledFn enc = encode_tiled();
+  const long long rows = L < 256 ? L : 256;
+  if (!enc || L % rows || nx % W) return false;
+  cuuint64_t dims[5] = {(cuuint64_t)(2 * nx), (cuuint64_t)rows, (cuuint64_t)(L / rows), (cuuint64_t)nouter, 3};
+  cuuint64_t strides[4] = {(cuuint64_t)(line_stride * 16), (cuuint64_t)(line_stride * 16 * rows),
+                           (cuuint64_t)(outer_stride * 16), (cuuint64_t)(comp_stride * 16)};
+  cuuint32_t box[5] = {(cuuint32_t)(2 * W), (cuuint32_t)rows, (cuuint32_t)(L / rows), 1, 3};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("FFTC_VERBOSE")) fprintf(stderr, "[fftc] 5-D tensor map failed: %d\n", (int)r);
+  return r == CUDA_SUCCESS;
+}
+
+// one TMA 3-D column pass: tiles of W x-columns x `nouter` outer lines,
+// fields A (and B when given), all three components per tile
+struct Col3Pass {
+  const KInfo* k = nullptr;
+  Line3 g{};
+  CUtensorMap mA, mB;
+  long long tiles = 0;
+  bool ok = false;
+};
+bool col3_pass(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B, long long L, long long line_stride,
+               long long nouter, long long outer_stride, long long comp_stride, int nfields, int axis, int o0, int on) {
+  p.ok = false;
+  const char* sel = getenv("FFTC_TMA_COLS3");  // "0": the strip kernels (k_col), for comparison
+  if (!k.fn || k.max_active <= 0 || (sel && atoi(sel) == 0)) return false;
+  const int W = col3_tile_w(L);
+  if (!make_line_map(&p.mA, A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride)) return false;
+  if (!make_line_map(&p.mB, B ? B : A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride)) return false;
+  p.k = &k;
+  p.g.nouter = (int)nouter;
+  p.g.o0 = o0;
+  p.g.on = on;
+  p.g.nfields = nfields;
+  p.g.axis = axis;
+  p.tiles = nouter * (a.nx / W) * nfields;
+  p.ok = true;
+  return true;
+}
+
 double2 C2(const double* p) { return make_double2(p[0], p[1]); }
 double2 hmul(double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
 double2 hadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -446,7 +494,8 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   bool use_graph;
   {
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    use_graph = !g_profile && pr->max_iters <= (1 << 20) && !getenv("FFTC_NO_GRAPH");
+    // (FFTC_DEBUG_SYNC synchronises after every launch: not allowed in a capture)
+    use_graph = !g_profile && pr->max_iters <= (1 << 20) && !getenv("FFTC_NO_GRAPH") && !debug_sync();
   }
   // graph mode runs the whole loop in one launch: the device keeps every record
   const int hist_ring = use_graph ? (int)std::max<int64_t>(pr->max_iters, 16) : 1024;
@@ -545,6 +594,15 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       yf.ostride = nx * ny;
       yf.nstrips = (int)(nx / 2);
     }
+    // 3-D TMA column passes (cols3_tma.cuh) where the line lengths allow
+    Col3Pass zmid, yfwd, yinv;
+    if (d == 3) {
+      col3_pass(zmid, TZ.col[em_type ? KC_MID3T_EM : KC_MID3T_BASIC], a, a.A, em_type ? a.B : nullptr, nz, nx * ny, ny,
+                nx, N, em_type ? 2 : 1, 2, 0, (int)ny);
+      col3_pass(yfwd, TY.col[KC_FWD3T], a, a.A, em_type ? a.B : nullptr, ny, nx, nz, nx * ny, N, em_type ? 2 : 1, 1, 0,
+                (int)nz);
+      col3_pass(yinv, TY.col[KC_INV3T], a, a.A, nullptr, ny, nx, nz, nx * ny, N, 1, 1, 0, (int)nz);
+    }
     const long long mid_lines = use_tma_mid ? nx * (em_type ? 2 : 1)
                                             : (long long)mid.nouter * mid.nstrips * (em_type ? 2 : 1);
     const long long row_lines = (long long)d * ny * nz;
@@ -560,20 +618,35 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       int r = L.go(TX.s1[scheme], row_lines, a1, K_SWEEP1);
       if (r) return r;
       if (d == 3) {
-        // y forward of field A (and B for em-type) -- plain column pass
-        Args aB = a;
-        void* ayf[] = {&a, &yf};
-        if ((r = L.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD))) return r;
-        if (em_type) {
-          aB.A = a.B;
-          void* ab[] = {&aB, &yfB};
-          if ((r = L.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD))) return r;
+        // y forward of field A (and B for em-type)
+        if (yfwd.ok) {
+          void* ay[] = {&a, &yfwd.g, &yfwd.mA, &yfwd.mB};
+          if ((r = L.go(*yfwd.k, yfwd.tiles, ay, K_YFWD))) return r;
+        } else {
+          Args aB = a;
+          void* ayf[] = {&a, &yf};
+          if ((r = L.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD))) return r;
+          if (em_type) {
+            aB.A = a.B;
+            void* ab[] = {&aB, &yfB};
+            if ((r = L.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD))) return r;
+          }
         }
       }
-      if ((r = L.go(*kmid, mid_lines, amid, K_MID))) return r;
+      if (d == 3 && zmid.ok) {
+        void* az[] = {&a, &zmid.g, &zmid.mA, &zmid.mB};
+        if ((r = L.go(*zmid.k, zmid.tiles, az, K_MID))) return r;
+      } else if ((r = L.go(*kmid, mid_lines, amid, K_MID))) {
+        return r;
+      }
       if (d == 3) {
-        void* ai[] = {&a, &yf};
-        if ((r = L.go(TY.col[KC_INV], yf_lines, ai, K_YINV))) return r;
+        if (yinv.ok) {
+          void* ay[] = {&a, &yinv.g, &yinv.mA, &yinv.mB};
+          if ((r = L.go(*yinv.k, yinv.tiles, ay, K_YINV))) return r;
+        } else {
+          void* ai[] = {&a, &yf};
+          if ((r = L.go(TY.col[KC_INV], yf_lines, ai, K_YINV))) return r;
+        }
       }
       return L.go(TX.s3[scheme], row_lines, a1, K_SWEEP3);
     };
@@ -1030,6 +1103,7 @@ struct fftc_slab {
   char* ws = nullptr;
   double* tot_dev = nullptr;  // 8 doubles of host-supplied totals
   DevState* hst = nullptr;
+  Col3Pass yfwd3, yinv3, mid3;  // TMA tile column passes where the lengths allow
 };
 
 int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, void* Bz, void* Ay, void* By,
@@ -1114,6 +1188,16 @@ int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, 
   sl->zg.nstrips = (int)(nx / R.tab[lgz].col3_w);
   sl->zg.o0 = (int)sd->y0;
   sl->zg.on = (int)ny;
+  {
+    const LTable& TY = R.tab[lgy];
+    const LTable& TZ = R.tab[lgz];
+    const int nf = sl->em_type ? 2 : 1;
+    col3_pass(sl->yfwd3, TY.col[KC_FWD3T], a, Az, sl->em_type ? Bz : nullptr, ny, nx, sd->nzl, nx * ny, N_l, nf, 1,
+              0, (int)sd->nzl);
+    col3_pass(sl->yinv3, TY.col[KC_INV3T], a, Az, nullptr, ny, nx, sd->nzl, nx * ny, N_l, 1, 1, 0, (int)sd->nzl);
+    col3_pass(sl->mid3, TZ.col[sl->em_type ? KC_MID3T_EM : KC_MID3T_BASIC], sl->mid, Ay, sl->em_type ? By : nullptr,
+              nz, nx, sd->nyl, nz * nx, sd->nyl * nz * nx, nf, 2, (int)sd->y0, (int)ny);
+  }
   if (cudaMallocHost((void**)&sl->hst, sizeof(DevState)) != cudaSuccess ||
       cudaMemsetAsync(a.st, 0, sizeof(DevState), s) != cudaSuccess) {
     g_err = "slab: state allocation failed";
@@ -1167,13 +1251,18 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
     }
     case FFTC_SLAB_ROWS_FWD: {
       if ((rc = Lc.go(TX.s1[sl->scheme], (long long)d * rows, a1, K_SWEEP1))) return rc;
-      void* ayf[] = {&a, &sl->yf};
-      if ((rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD))) return rc;
-      if (sl->em_type) {
-        Args aB = a;
-        aB.A = a.B;
-        void* ab[] = {&aB, &sl->yf};
-        if ((rc = Lc.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD))) return rc;
+      if (sl->yfwd3.ok) {
+        void* ay[] = {&a, &sl->yfwd3.g, &sl->yfwd3.mA, &sl->yfwd3.mB};
+        if ((rc = Lc.go(*sl->yfwd3.k, sl->yfwd3.tiles, ay, K_YFWD))) return rc;
+      } else {
+        void* ayf[] = {&a, &sl->yf};
+        if ((rc = Lc.go(TY.col[KC_FWD], yf_lines, ayf, K_YFWD))) return rc;
+        if (sl->em_type) {
+          Args aB = a;
+          aB.A = a.B;
+          void* ab[] = {&aB, &sl->yf};
+          if ((rc = Lc.go(TY.col[KC_FWD], yf_lines, ab, K_YFWD))) return rc;
+        }
       }
       if (slab_read_state(sl, s)) return 1;
       for (int c = 0; c < 3; ++c) {
@@ -1184,17 +1273,27 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
       return 0;
     }
     case FFTC_SLAB_MID: {
-      const KInfo& k = TZ.col[sl->em_type ? KC_MID3_EM : KC_MID3_BASIC];
-      void* am[] = {&sl->mid, &sl->zg};
-      const long long lines = (long long)sl->zg.nouter * sl->zg.nstrips * (sl->em_type ? 2 : 1);
-      if ((rc = Lc.go(k, lines, am, K_MID))) return rc;
+      if (sl->mid3.ok) {
+        void* am[] = {&sl->mid, &sl->mid3.g, &sl->mid3.mA, &sl->mid3.mB};
+        if ((rc = Lc.go(*sl->mid3.k, sl->mid3.tiles, am, K_MID))) return rc;
+      } else {
+        const KInfo& k = TZ.col[sl->em_type ? KC_MID3_EM : KC_MID3_BASIC];
+        void* am[] = {&sl->mid, &sl->zg};
+        const long long lines = (long long)sl->zg.nouter * sl->zg.nstrips * (sl->em_type ? 2 : 1);
+        if ((rc = Lc.go(k, lines, am, K_MID))) return rc;
+      }
       if (slab_read_state(sl, s)) return 1;
       out[0] = sl->hst->parseval;
       return 0;
     }
     case FFTC_SLAB_ROWS_INV: {
-      void* ai[] = {&a, &sl->yf};
-      if ((rc = Lc.go(TY.col[KC_INV], yf_lines, ai, K_YINV))) return rc;
+      if (sl->yinv3.ok) {
+        void* ay[] = {&a, &sl->yinv3.g, &sl->yinv3.mA, &sl->yinv3.mB};
+        if ((rc = Lc.go(*sl->yinv3.k, sl->yinv3.tiles, ay, K_YINV))) return rc;
+      } else {
+        void* ai[] = {&a, &sl->yf};
+        if ((rc = Lc.go(TY.col[KC_INV], yf_lines, ai, K_YINV))) return rc;
+      }
       if ((rc = Lc.go(TX.s3[sl->scheme], (long long)d * rows, a1, K_SWEEP3))) return rc;
       if (slab_read_state(sl, s)) return 1;
       for (int c = 0; c < 3; ++c) {

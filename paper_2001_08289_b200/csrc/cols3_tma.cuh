@@ -1,0 +1,176 @@
+// cols3_tma.cuh -- TMA-staged column passes of 3-D fields (the y passes and
+// the z pass with the Gamma projection) for line lengths 256..1024.
+//
+// Same algebra as k_col (sweeps.cuh): the 3-D Gamma_1 of
+// spectral_ops.py:120-128 (a third wave-vector component) and the plain y
+// transforms around it.  Data movement:
+//   * a tile is W adjacent x-columns of all three components along the
+//     line axis; ONE cp.async.bulk.tensor copy of a 5-D tensor map {2*nx
+//     doubles, 256-row block, L/256 blocks, outer index, component} with box
+//     {2W, 256, L/256, 1, 3} lands it in shared memory as [c][pos][w] --
+//     whatever the line stride (z: nx*ny, y: nx).  W is chosen so a box row
+//     is 64..128 B: one-column boxes (16 B rows) run into the TMA request
+//     rate and, along z, touch a new 2 MB page per 16 bytes;
+//   * one tile per CTA at a time (3*W*T = 768 threads, radix 8, 16 data
+//     registers per thread), two slots: tile j+1 streams in while tile j is
+//     transformed, tile j leaves by TMA store while tile j+1 starts;
+//   * the slot is the FFT exchange area once the inputs are in registers;
+//     the projection's k.F^ crosses the component warps through it.
+// Tiles are numbered x fastest, so concurrent CTAs work on neighbouring
+// columns of the same rows.
+#pragma once
+#include "cols_tma.cuh"
+
+namespace fftc {
+
+template <int L>
+struct Col3Tma {
+  static constexpr int E = 8;
+  static constexpr int T = L / E;
+  static constexpr int W = L <= 256 ? 8 : (L <= 512 ? 4 : 2);  // columns per tile
+  static constexpr int NC = 3;
+  static constexpr int THREADS = NC * W * T;
+  static constexpr int LP = Plan<L, E>::LP;
+  // per (component, column) exchange stride: the W buffers start in distinct
+  // 16-B bank groups, and SLOT stays a multiple of 8 entries (128 B)
+  static constexpr int XS = LP + (W == 2 ? 4 : 2);
+  static constexpr int SLOT = NC * W * XS;  // >= NC*W*L landing
+  static constexpr int NSLOT = 2;
+  static constexpr int SMEM = (NSLOT * SLOT + L / 2) * (int)sizeof(double2);
+  static constexpr int BOXR = L < 256 ? L : 256;
+  static constexpr unsigned TX = (unsigned)(NC * W * L * sizeof(double2));
+  static_assert(THREADS <= 1024, "block size");
+  static_assert((SLOT * 16) % 128 == 0, "TMA destinations stay 128-B aligned");
+  static_assert(SMEM <= 232448 - 512, "shared memory budget");
+};
+
+__device__ __forceinline__ void col3_issue(const CUtensorMap* tm, double2* slot, uint64_t* bar, int x0, int o,
+                                           unsigned tx) {
+  bulk_wait_read0();  // the TMA store that last used this slot has read it out
+  mbar_expect_tx(bar, tx);
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(smem_u32(slot)),
+      "l"(tm), "r"(2 * x0), "r"(0), "r"(0), "r"(o), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2* slot, int x0, int o) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(tm),
+               "r"(2 * x0), "r"(0), "r"(0), "r"(o), "r"(0), "r"(smem_u32(slot))
+               : "memory");
+}
+
+template <int MODE, int L>
+__global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
+    k_col3_tma(Args a, Line3 g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+  using K = Col3Tma<L>;
+  constexpr int E = K::E, T = K::T, W = K::W;
+  constexpr bool MID = (MODE == MID_BASIC || MODE == MID_EM);
+  constexpr bool INV_ONLY = (MODE == COL_INV);
+  extern __shared__ __align__(128) double2 smem[];
+  __shared__ uint64_t bars[K::NSLOT];
+  if (!a.op_mode && a.st->stopped) return;
+  const int w = threadIdx.x % W, t = (threadIdx.x / W) % T, comp = threadIdx.x / (W * T);
+  const int nstrips = a.nx / W;
+  const long long per_field = (long long)g.nouter * nstrips;
+  const long long tiles = per_field * g.nfields;
+  const long long nmine = blockIdx.x < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto coords = [&](long long k, int& f, int& o, int& x0) {
+    const long long tile = blockIdx.x + k * gridDim.x;
+    f = (int)(tile / per_field);
+    const long long r = tile - (long long)f * per_field;
+    o = (int)(r / nstrips);
+    x0 = (int)(r - (long long)o * nstrips) * W;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < K::NSLOT; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && nmine > 0) {
+    int f, o, x0;
+    coords(0, f, o, x0);
+    col3_issue(f == 0 ? &tmA : &tmB, smem, &bars[0], x0, o, K::TX);
+  }
+  double2* tws = smem + K::NSLOT * K::SLOT;
+  for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[g.axis][i]);
+  __syncthreads();
+  const SmemTw tw{tws};
+  double acc = 0.0;
+  for (long long k = 0; k < nmine; ++k) {
+    const int s = (int)(k & 1);
+    int f, o, x0;
+    coords(k, f, o, x0);
+    double2* slot = smem + s * K::SLOT;
+    mbar_wait(&bars[s], (unsigned)((k >> 1) & 1));
+    double2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[0][i] = slot[(comp * L + pos_first<L, E>(INV_ONLY, t, i)) * W + w];
+    __syncthreads();  // every input is in registers: the slot becomes exchange scratch
+    if (threadIdx.x == 0 && k + 1 < nmine) {
+      // tile k+1 into the other slot, whose store (tile k-1) was committed one tile ago
+      int nf, no, nx0;
+      coords(k + 1, nf, no, nx0);
+      col3_issue(nf == 0 ? &tmA : &tmB, smem + (s ^ 1) * K::SLOT, &bars[s ^ 1], nx0, no, K::TX);
+    }
+    double2* xb = slot + (comp * W + w) * K::XS;
+    const bool parseval_only = (MODE == MID_EM) && f == 1;
+    if constexpr (!INV_ONLY) fft_line<L, E, 1, false>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
+    if constexpr (MID) {
+      // Gamma projection (spectral_ops.py:124-127), k = (kx, k_outer, k_line)
+      // for the components (x, y, z); k.F^ gathered across the component warps
+      const double kx = (double)wavenum(x0 + w, a.nx), ko = (double)wavenum(g.o0 + o, g.on);
+      __syncthreads();  // last exchange reads are done before kf overwrites the buffers
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int pos = pos_last<L, E>(false, t, i);
+        const double kc = comp == 0 ? kx : (comp == 1 ? ko : (double)wavenum(pos, L));
+        slot[(comp * L + pos) * W + w] = cscale(v[0][i], kc);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int pos = pos_last<L, E>(false, t, i);
+        const double kl = (double)wavenum(pos, L);
+        const double kc = comp == 0 ? kx : (comp == 1 ? ko : kl);
+        const double k2 = kx * kx + ko * ko + kl * kl;
+        const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
+        double2 dot = cadd(cadd(slot[pos * W + w], slot[(L + pos) * W + w]), slot[(2 * L + pos) * W + w]);
+        dot = cscale(dot, ik2);
+        if (MODE == MID_BASIC || parseval_only) {
+          const double2 gc = cscale(dot, kc);
+          acc += cabs2(cscale(gc, a.inv_n));  // Parseval on the 1/N-scaled mode
+          v[0][i] = gc;
+        } else {
+          v[0][i] = csub(v[0][i], cscale(dot, 2.0 * kc));
+        }
+      }
+      __syncthreads();  // kf reads are done before the inverse transform's exchanges
+    }
+    if (!parseval_only) {
+      if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
+      __syncthreads();  // every exchange read is done before outputs overwrite the slot
+      const bool inv_layout = (MODE != COL_FWD);
+#pragma unroll
+      for (int i = 0; i < E; ++i) slot[(comp * L + pos_last<L, E>(inv_layout, t, i)) * W + w] = v[0][i];
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        col3_store(f == 0 ? &tmA : &tmB, slot, x0, o);
+        bulk_commit();
+      }
+    } else {
+      __syncthreads();  // the slot is consumed
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait0();  // stores have landed in global memory
+  if constexpr (MID) {
+    double in[1] = {acc}, tot[1];
+    if (grid_reduce<1>(in, tot, a) && threadIdx.x == 0 && !a.op_mode) {
+      if (a.dist) a.st->parseval = tot[0] / a.inv_n;
+      else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
+    }
+  }
+}
+
+}  // namespace fftc

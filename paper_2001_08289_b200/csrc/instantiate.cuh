@@ -4,6 +4,7 @@
 #include "sweeps.cuh"
 #include "rows_tma.cuh"
 #include "cols_tma.cuh"
+#include "cols3_tma.cuh"
 #include "kernel_table.h"
 
 #ifndef FFTC_TMA_ROWS_MIN
@@ -70,6 +71,14 @@ inline void fill_tma(LTable& t) {
   if constexpr (LL >= 256 && LL <= 2048) {  // TMA tensor-map 2-D projection sweep
     t.col[KC_MID2T_BASIC] = make(k_mid2_tma<MID_BASIC, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
     t.col[KC_MID2T_EM] = make(k_mid2_tma<MID_EM, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
+  }
+  if constexpr (LL >= 256 && LL <= 1024) {  // TMA tensor-map 3-D column passes
+    using K3 = Col3Tma<LL>;
+    static_assert(K3::W == col3_tile_w(LL), "host and device tile widths agree");
+    t.col[KC_MID3T_BASIC] = make(k_col3_tma<MID_BASIC, LL>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_MID3T_EM] = make(k_col3_tma<MID_EM, LL>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_FWD3T] = make(k_col3_tma<COL_FWD, LL>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_INV3T] = make(k_col3_tma<COL_INV, LL>, K3::THREADS, K3::SMEM, 1);
   }
   if constexpr (LL >= FFTC_TMA_ROWS_MIN) {  // TMA-staged persistent row sweeps
 #define FFTC_TMA(SCH)                                                                                   \

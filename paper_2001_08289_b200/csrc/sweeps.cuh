@@ -549,6 +549,15 @@ struct ColGeom {
   int pad;
 };
 
+// geometry of a TMA 3-D column pass (cols3_tma.cuh)
+struct Line3 {
+  int nouter;   // outer lines per field (z for the y passes, y for the z pass)
+  int o0, on;   // global index of outer 0 and the outer axis extent (wave numbers)
+  int nfields;  // 1, or 2 (fields A and B: EM-type schemes)
+  int axis;     // twiddle table of the line axis (1 = y, 2 = z)
+  int pad[3];
+};
+
 template <int MODE, int L, int E, int W, int C, int G>
 __global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
   using P = Plan<L, E>;

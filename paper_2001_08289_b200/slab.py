@@ -154,9 +154,16 @@ def _allreduce(vec: np.ndarray, dist, group, device) -> np.ndarray:
 _STATUS = {0: TerminationStatus.CONVERGED, 1: TerminationStatus.MAX_ITERS, 2: TerminationStatus.DIVERGED}
 
 
-def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend_factory=None) -> dict:
-    """Slab-decomposed solve of a 3-D cell; every rank returns the same record dict."""
-    dist, rank, world = _dist(group)
+def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend_factory=None, comm=None) -> dict:
+    """Slab-decomposed solve of a 3-D cell; every rank returns the same record dict.
+
+    `comm` (tests): an object with `rank`, `world`, `all_to_all_single(out,
+    inp, group=None)` and `all_reduce(t, group=None)` standing in for
+    torch.distributed."""
+    if comm is not None:
+        dist, rank, world = comm, comm.rank, comm.world
+    else:
+        dist, rank, world = _dist(group)
     chi_global = np.asarray(chi_global, dtype=bool)
     if chi_global.ndim != 3:
         raise ValueError("slab decomposition is for 3-D cells")
@@ -166,6 +173,8 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
     factory = backend_factory or GpuSlab
     be = factory(chi_global[z0:z0 + nzl], (nz, ny, nx), z0, nzl, y0, nyl, cfg)
     device = "cuda" if factory is GpuSlab else "cpu"
+    if world == 1:
+        dist = None
     e0 = cfg.e0_vector(3)
     e0v = np.array([[z.real, z.imag] for z in e0]).ravel()
     try:

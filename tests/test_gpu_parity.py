@@ -148,3 +148,26 @@ def test_repeat_determinism_long_em_sub():
     assert len(h0) == 1000
     for r in runs[1:]:
         assert [(h.sigma_star, h.residual) for h in r.history] == h0
+
+
+@pytest.mark.parametrize("shape, scheme", [((256, 256, 8), "em_sub"), ((256, 256, 8), "basic"),
+                                           ((512, 256, 4), "em"), ((1024, 256, 2), "basic_sub")])
+def test_3d_tma_column_passes_vs_oracle(shape, scheme):
+    """Grids whose y and z lines (256..1024) run the TMA tile kernels
+    (cols3_tma.cuh), against the oracle restatement (pinned to the reference
+    by the 2-D goldens and the 2-D embedding check)."""
+    import paper_2001_08289_b200 as fb
+    from oracle import fftcond_oracle as O
+
+    rng = np.random.default_rng(3)
+    chi = rng.random(shape) < 0.3
+    sk = fb.SchemeKind(scheme)
+    e0 = (0.6, 0.0, 0.8)
+    cfg = fb.SolverConfig(scheme=sk, sigma1=10.0 + 2j, tol=1e-8, max_iters=200, e0=e0,
+                          interval=fb.SpectralInterval(ALPHA, BETA) if sk.substituted else None)
+    r = fb.solve(fb.PhaseMap(chi), cfg)
+    ref = O.solve(chi, scheme, 10.0 + 2j, e0=e0, tol=1e-8, max_iters=200, alpha=ALPHA, beta=BETA)
+    assert r.iterations == len(ref.history) and r.status.value == ref.status
+    for h, (_, s, res) in zip(r.history, ref.history):
+        assert abs(h.sigma_star - s) <= 1e-10 * abs(s)
+        assert abs(h.residual - res) <= 1e-6 * res
