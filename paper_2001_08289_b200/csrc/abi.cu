@@ -130,7 +130,10 @@ int ensure_registry() {
         }
       }
       int nb = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k->fn, k->threads, k->smem));
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k->fn, k->threads, k->smem) != cudaSuccess) {
+        cudaGetLastError();  // e.g. a configuration this device cannot run: leave it unusable
+        nb = 0;
+      }
       k->max_active = nb;
     }
     if (!r.tw[lg]) {

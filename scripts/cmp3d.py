@@ -11,6 +11,7 @@ import paper_2001_08289_b200 as fb  # noqa: E402
 shapes = [tuple(int(v) for v in s.split("x")) for s in (sys.argv[1].split(",") if len(sys.argv) > 1 else
                                                         ["256x256x8", "512x256x4", "256x1024x2", "1024x256x2"])]
 schemes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["basic", "em", "basic_sub", "em_sub"]
+VAR = "FFTC_TMA_COLS3"  # TMA tile passes ("1") vs the strip kernels ("0")
 iv = fb.SpectralInterval(0.25, 4.0)
 bad = 0
 for shape in shapes:
@@ -20,9 +21,9 @@ for shape in shapes:
         sk = fb.SchemeKind(scheme)
         cfg = fb.SolverConfig(scheme=sk, sigma1=10.0 + 2j, tol=1e-10, max_iters=300, e0=(0.6, 0.0, 0.8),
                               interval=iv if sk.substituted else None)
-        os.environ["FFTC_TMA_COLS3"] = "0"
+        os.environ[VAR] = "0"
         r0 = fb.solve(pm, cfg)
-        os.environ["FFTC_TMA_COLS3"] = "1"
+        os.environ[VAR] = "1"
         r1 = fb.solve(pm, cfg)
         h0 = np.array([[h.sigma_star.real, h.sigma_star.imag, h.residual] for h in r0.history])
         h1 = np.array([[h.sigma_star.real, h.sigma_star.imag, h.residual] for h in r1.history])
