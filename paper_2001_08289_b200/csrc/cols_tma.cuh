@@ -71,12 +71,6 @@ __device__ __forceinline__ void cols_tma_issue(const CUtensorMap* tm, double2* s
   tma_load_4d(slot, tm, 2 * x, 0, 0, 0, bar);
 }
 
-struct HalfSync {
-  int id;
-  int n;
-  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-};
-
 #ifdef FFTC_PHASE_TIMING
 #define PHASE_MARK(i)                                                                            \
   do {                                                                                           \

@@ -196,7 +196,13 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
     }
     __syncthreads();  // the main row becomes exchange scratch
     double2* xb = (CH == 2 && ch == 1) ? (K::ST_ROWS ? st + K::ST_OFF : xbuf) : st;
-    fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
+    if constexpr (CH == 2) {
+      // the two channels transform in separate buffers: each synchronises
+      // only its own T threads (named barrier 1 + ch), not the whole CTA
+      fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, HalfSync{1 + ch, T});
+    } else {
+      fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
+    }
     if constexpr (SW == 1) {
 #pragma unroll
       for (int i = 0; i < E; ++i) OUT[off + pos_last<L, E>(false, t, i)] = v[0][i];

@@ -290,6 +290,12 @@ struct SmemBuf {
 struct SyncAll {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
+// named barrier over n threads (a multiple of 32) -- a group of warps
+struct HalfSync {
+  int id;
+  int n;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+};
 
 // L2 prefetch of everything a row sweep reads for line `ln` = (c, row).
 // S/T slots are fetched only over the row's phase-1 extent.
