@@ -122,6 +122,16 @@ int fftc_slab_set_delta(fftc_slab* slab, const double* delta6, void* stream);
 int fftc_slab_monitor(fftc_slab* slab, const double* totals8, double* record7, void* stream);
 int fftc_slab_finalize(fftc_slab* slab, void* E, void* J, void* aug, double* means12, void* stream);
 void fftc_slab_destroy(fftc_slab* slab);
+/* Fused transposes (NVLink peer memory): after this call the y forward pass
+ * of FFTC_SLAB_ROWS_FWD writes its output rows directly into the y-slab
+ * buffers of their owning ranks, and FFTC_SLAB_MID writes its result back
+ * into the owning ranks' z-slab buffers, so the caller skips both
+ * all-to-alls and only orders the phases (a barrier after ROWS_FWD; the
+ * all-reduce after MID).  Ay, Az (and By for em / em_sub): `world` device
+ * pointers, rank order, peer-accessible from this rank.  Returns 3 when the
+ * grid cannot use the fused passes (y and z lines of 256..1024). */
+int fftc_slab_set_peers(fftc_slab* slab, int32_t world, void* const* Ay, void* const* By, void* const* Az,
+                        void* stream);
 
 /* Same contract, host-resident chi and outputs (the library copies in and
  * out; E/J/aug host buffers are nullable).  For FFI users without a device

@@ -599,6 +599,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     }
     // 3-D TMA column passes (cols3_tma.cuh) where the line lengths allow
     Col3Pass zmid, yfwd, yinv;
+    const PeerOut* no_peer = nullptr;
     if (d == 3) {
       col3_pass(zmid, TZ.col[em_type ? KC_MID3T_EM : KC_MID3T_BASIC], a, a.A, em_type ? a.B : nullptr, nz, nx * ny, ny,
                 nx, N, em_type ? 2 : 1, 2, 0, (int)ny);
@@ -623,7 +624,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       if (d == 3) {
         // y forward of field A (and B for em-type)
         if (yfwd.ok) {
-          void* ay[] = {&a, &yfwd.g, &yfwd.mA, &yfwd.mB};
+          void* ay[] = {&a, &yfwd.g, &yfwd.mA, &yfwd.mB, &no_peer};
           if ((r = L.go(*yfwd.k, yfwd.tiles, ay, K_YFWD))) return r;
         } else {
           Args aB = a;
@@ -637,14 +638,14 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
         }
       }
       if (d == 3 && zmid.ok) {
-        void* az[] = {&a, &zmid.g, &zmid.mA, &zmid.mB};
+        void* az[] = {&a, &zmid.g, &zmid.mA, &zmid.mB, &no_peer};
         if ((r = L.go(*zmid.k, zmid.tiles, az, K_MID))) return r;
       } else if ((r = L.go(*kmid, mid_lines, amid, K_MID))) {
         return r;
       }
       if (d == 3) {
         if (yinv.ok) {
-          void* ay[] = {&a, &yinv.g, &yinv.mA, &yinv.mB};
+          void* ay[] = {&a, &yinv.g, &yinv.mA, &yinv.mB, &no_peer};
           if ((r = L.go(*yinv.k, yinv.tiles, ay, K_YINV))) return r;
         } else {
           void* ai[] = {&a, &yf};
@@ -1107,6 +1108,9 @@ struct fftc_slab {
   double* tot_dev = nullptr;  // 8 doubles of host-supplied totals
   DevState* hst = nullptr;
   Col3Pass yfwd3, yinv3, mid3;  // TMA tile column passes where the lengths allow
+  long long z0 = 0, nyl = 0;    // this rank's first z-plane and y-slab height
+  bool fused = false;           // transposes fused into the y forward / z passes (fftc_slab_set_peers)
+  PeerOut* po_dev = nullptr;    // [0]: y forward -> y-slabs, [1]: z pass -> z-slabs
 };
 
 int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, void* Bz, void* Ay, void* By,
@@ -1175,6 +1179,8 @@ int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, 
   a.tw[2] = R.tw[lgz];
   sl->mid = a;
   sl->mid.nz = (int)nz;  // the z pass sees whole z lines
+  sl->z0 = sd->z0;
+  sl->nyl = sd->nyl;
   sl->mid.A = (double2*)Ay;
   sl->mid.B = sl->em_type ? (double2*)By : (double2*)Ay;
   // y passes on the z-slab (lines along y, one per (z, x-strip, component))
@@ -1254,8 +1260,15 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
     }
     case FFTC_SLAB_ROWS_FWD: {
       if ((rc = Lc.go(TX.s1[sl->scheme], (long long)d * rows, a1, K_SWEEP1))) return rc;
-      if (sl->yfwd3.ok) {
-        void* ay[] = {&a, &sl->yfwd3.g, &sl->yfwd3.mA, &sl->yfwd3.mB};
+      if (sl->fused) {
+        // y forward with its output rows written straight into the owning
+        // ranks' y-slabs: this pass IS the forward transpose
+        const PeerOut* po = sl->po_dev;
+        void* ay[] = {&a, &sl->yfwd3.g, &sl->yfwd3.mA, &sl->yfwd3.mB, &po};
+        if ((rc = Lc.go(TY.col[KC_FWD3P], sl->yfwd3.tiles, ay, K_YFWD))) return rc;
+      } else if (sl->yfwd3.ok) {
+        const PeerOut* no_peer = nullptr;
+        void* ay[] = {&a, &sl->yfwd3.g, &sl->yfwd3.mA, &sl->yfwd3.mB, &no_peer};
         if ((rc = Lc.go(*sl->yfwd3.k, sl->yfwd3.tiles, ay, K_YFWD))) return rc;
       } else {
         void* ayf[] = {&a, &sl->yf};
@@ -1276,8 +1289,14 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
       return 0;
     }
     case FFTC_SLAB_MID: {
-      if (sl->mid3.ok) {
-        void* am[] = {&sl->mid, &sl->mid3.g, &sl->mid3.mA, &sl->mid3.mB};
+      if (sl->fused) {
+        // z pass writing back into the owning ranks' z-slabs: the backward transpose
+        const PeerOut* po = sl->po_dev + 1;
+        void* am[] = {&sl->mid, &sl->mid3.g, &sl->mid3.mA, &sl->mid3.mB, &po};
+        if ((rc = Lc.go(TZ.col[sl->em_type ? KC_MID3P_EM : KC_MID3P_BASIC], sl->mid3.tiles, am, K_MID))) return rc;
+      } else if (sl->mid3.ok) {
+        const PeerOut* no_peer = nullptr;
+        void* am[] = {&sl->mid, &sl->mid3.g, &sl->mid3.mA, &sl->mid3.mB, &no_peer};
         if ((rc = Lc.go(*sl->mid3.k, sl->mid3.tiles, am, K_MID))) return rc;
       } else {
         const KInfo& k = TZ.col[sl->em_type ? KC_MID3_EM : KC_MID3_BASIC];
@@ -1291,7 +1310,8 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
     }
     case FFTC_SLAB_ROWS_INV: {
       if (sl->yinv3.ok) {
-        void* ay[] = {&a, &sl->yinv3.g, &sl->yinv3.mA, &sl->yinv3.mB};
+        const PeerOut* no_peer = nullptr;
+        void* ay[] = {&a, &sl->yinv3.g, &sl->yinv3.mA, &sl->yinv3.mB, &no_peer};
         if ((rc = Lc.go(*sl->yinv3.k, sl->yinv3.tiles, ay, K_YINV))) return rc;
       } else {
         void* ai[] = {&a, &sl->yf};
@@ -1376,9 +1396,57 @@ int fftc_slab_finalize(fftc_slab* sl, void* E, void* J, void* aug, double* means
   return 0;
 }
 
+int fftc_slab_set_peers(fftc_slab* sl, int32_t world, void* const* Ay, void* const* By, void* const* Az,
+                        void* stream) {
+  g_err.clear();
+  if (!sl || !Ay || !Az || world < 1 || world > 8 || (sl->em_type && !By)) {
+    g_err = "slab peers: null argument or world outside 1..8";
+    return 2;
+  }
+  const Args& a = sl->row;
+  const long long nx = a.nx, ny = a.ny, nzl = a.nz, nz = sl->mid.nz, nyl = sl->nyl;
+  if (ny % world || nz % world || ny / world != nyl || nz / world != nzl) {
+    g_err = "slab peers: world does not match the slab geometry";
+    return 2;
+  }
+  Registry& R = reg();
+  const bool kernels = R.tab[sl->lgy].col[KC_FWD3P].max_active > 0 &&
+                       R.tab[sl->lgz].col[sl->em_type ? KC_MID3P_EM : KC_MID3P_BASIC].max_active > 0;
+  if (!sl->yfwd3.ok || !sl->mid3.ok || !kernels) {
+    g_err = "slab peers: fused transposes need y and z lines of 256..1024 (TMA tile passes)";
+    return 3;
+  }
+  PeerOut po[2];
+  memset(po, 0, sizeof(po));
+  for (int q = 0; q < world; ++q) {
+    po[0].dst[0][q] = (double2*)Ay[q];  // y forward -> y-slab (c, y_l, z, x) of rank q
+    po[0].dst[1][q] = (double2*)(sl->em_type ? By[q] : Ay[q]);
+    po[1].dst[0][q] = (double2*)Az[q];  // z pass -> z-slab (c, z_l, y, x) of rank q
+    po[1].dst[1][q] = (double2*)Az[q];
+  }
+  po[0].world = po[1].world = world;
+  po[0].rows_per_rank = (int)nyl;
+  po[0].line_stride = nz * nx;  // y_l
+  po[0].outer_stride = nx;      // z
+  po[0].outer0 = sl->z0;        // z of this rank's plane z_l
+  po[0].comp_stride = nyl * nz * nx;
+  po[1].rows_per_rank = (int)nzl;
+  po[1].line_stride = ny * nx;  // z_l
+  po[1].outer_stride = nx;      // y
+  po[1].outer0 = sl->zg.o0;     // y0
+  po[1].comp_stride = nzl * ny * nx;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!sl->po_dev) CK(cudaMalloc((void**)&sl->po_dev, sizeof(po)));
+  CK(cudaMemcpyAsync(sl->po_dev, po, sizeof(po), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  sl->fused = true;
+  return 0;
+}
+
 void fftc_slab_destroy(fftc_slab* sl) {
   if (!sl) return;
   cudaDeviceSynchronize();
+  if (sl->po_dev) cudaFree(sl->po_dev);
   if (sl->ws) cudaFree(sl->ws);
   if (sl->hst) cudaFreeHost(sl->hst);
   delete sl;

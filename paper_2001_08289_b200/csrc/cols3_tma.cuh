@@ -60,9 +60,13 @@ __device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2*
                : "memory");
 }
 
-template <int MODE, int L>
+// PEER: outputs are written straight to their owning rank (PeerOut po,
+// device memory) instead of back through the slot and a TMA store -- the
+// decomposed solve's transposes fused into the pass that produces the data.
+template <int MODE, int L, bool PEER = false>
 __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
-    k_col3_tma(Args a, Line3 g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    k_col3_tma(Args a, Line3 g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const PeerOut* __restrict__ po) {
   using K = Col3Tma<L>;
   constexpr int E = K::E, T = K::T, W = K::W;
   constexpr bool MID = (MODE == MID_BASIC || MODE == MID_EM);
@@ -147,7 +151,19 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
       }
       __syncthreads();  // kf reads are done before the inverse transform's exchanges
     }
-    if (!parseval_only) {
+    if (PEER && !parseval_only) {
+      if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
+      const bool inv_layout = (MODE != COL_FWD);
+      const int rq = po->rows_per_rank;
+      const long long base = comp * po->comp_stride + (po->outer0 + o) * po->outer_stride + x0 + w;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int pos = pos_last<L, E>(inv_layout, t, i);
+        const int q = pos / rq;
+        po->dst[f][q][base + (long long)(pos - q * rq) * po->line_stride] = v[0][i];
+      }
+      __syncthreads();  // the slot's exchange reads are done before the next tile lands
+    } else if (!parseval_only) {
       if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
       __syncthreads();  // every exchange read is done before outputs overwrite the slot
       const bool inv_layout = (MODE != COL_FWD);
@@ -164,6 +180,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
     }
   }
   if (threadIdx.x == 0) bulk_wait0();  // stores have landed in global memory
+  if constexpr (PEER) __threadfence_system();  // peer stores visible before the host-level barrier
   if constexpr (MID) {
     double in[1] = {acc}, tot[1];
     if (grid_reduce<1>(in, tot, a) && threadIdx.x == 0 && !a.op_mode) {

@@ -79,6 +79,9 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID3T_EM] = make(k_col3_tma<MID_EM, LL>, K3::THREADS, K3::SMEM, 1);
     t.col[KC_FWD3T] = make(k_col3_tma<COL_FWD, LL>, K3::THREADS, K3::SMEM, 1);
     t.col[KC_INV3T] = make(k_col3_tma<COL_INV, LL>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_MID3P_BASIC] = make(k_col3_tma<MID_BASIC, LL, true>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_MID3P_EM] = make(k_col3_tma<MID_EM, LL, true>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_FWD3P] = make(k_col3_tma<COL_FWD, LL, true>, K3::THREADS, K3::SMEM, 1);
   }
   if constexpr (LL >= FFTC_TMA_ROWS_MIN) {  // TMA-staged persistent row sweeps
 #define FFTC_TMA(SCH)                                                                                   \

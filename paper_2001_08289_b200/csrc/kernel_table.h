@@ -16,8 +16,9 @@ struct KInfo {
 // column kernel variants
 enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_FWD = 4, KC_INV = 5,
        KC_MID2T_BASIC = 6, KC_MID2T_EM = 7,  // *T: TMA tensor-map variants (signature Args, map A, map B)
-       KC_MID3T_BASIC = 8, KC_MID3T_EM = 9, KC_FWD3T = 10, KC_INV3T = 11,  // 3-D (Args, Line3, map A, map B)
-       KC_COUNT = 12 };
+       KC_MID3T_BASIC = 8, KC_MID3T_EM = 9, KC_FWD3T = 10, KC_INV3T = 11,  // 3-D (Args, Line3, map A, map B, PeerOut*)
+       KC_MID3P_BASIC = 12, KC_MID3P_EM = 13, KC_FWD3P = 14,  // the same, outputs to their owning ranks
+       KC_COUNT = 15 };
 // columns per TMA tile of the 3-D column passes (cols3_tma.cuh: Col3Tma<L>::W)
 constexpr int col3_tile_w(long long L) { return L <= 256 ? 8 : (L <= 512 ? 4 : 2); }
 

@@ -564,6 +564,18 @@ struct Line3 {
   int pad[3];
 };
 
+// Destinations of a column pass whose outputs go straight to the rank that
+// owns them (fused z-slab <-> y-slab transposes of the decomposed 3-D solve,
+// peer memory over NVLink): element (c, line position pos, x) of the tile at
+// outer index o lands in rank q = pos / rows_per_rank at
+//   dst[field][q] + c*comp_stride + (outer0 + o)*outer_stride
+//                 + (pos - q*rows_per_rank)*line_stride + x.
+struct PeerOut {
+  double2* dst[2][8];
+  int world, rows_per_rank;
+  long long line_stride, outer_stride, outer0, comp_stride;
+};
+
 template <int MODE, int L, int E, int W, int C, int G>
 __global__ void __launch_bounds__(G*W*(L / E)) k_col(Args a, ColGeom gm) {
   using P = Plan<L, E>;

@@ -30,6 +30,7 @@ EXPORTS = (
     "fftc_aug_apply",
     "fftc_apply_sigma",
     "fftc_reduce",
+    "fftc_slab_set_peers",
     "fftc_profile",
     "fftc_kernel_stats",
     "fftc_solve_batch",
@@ -111,6 +112,8 @@ def lib():
         L.fftc_slab_monitor.restype = C.c_int
         L.fftc_slab_finalize.argtypes = [vp, vp, vp, vp, vp, vp]
         L.fftc_slab_finalize.restype = C.c_int
+        L.fftc_slab_set_peers.argtypes = [vp, C.c_int32, vp, vp, vp, vp]
+        L.fftc_slab_set_peers.restype = C.c_int
         L.fftc_slab_destroy.argtypes = [vp]
         L.fftc_slab_destroy.restype = None
         L.fftc_fft.argtypes = [C.POINTER(Problem), vp, C.c_int32, C.c_int32, vp]

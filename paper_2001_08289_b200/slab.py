@@ -99,6 +99,21 @@ class GpuSlab:
         self._call(self.L.fftc_slab_monitor, t.ctypes.data, rec.ctypes.data)
         return rec
 
+    def set_peers(self, world: int, ay, by, az) -> bool:
+        """Fused transposes: device pointers of every rank's A_y, B_y, A_z
+        (rank order, peer-accessible).  False when the grid cannot use them."""
+        arr = C.c_void_p * world
+        rc = self.L.fftc_slab_set_peers(self.h, world, arr(*ay), arr(*by) if self.em_type else None, arr(*az),
+                                        self._stream())
+        if rc == 3:
+            return False
+        if rc:
+            raise BackendError(f"fftc_slab_set_peers failed ({rc}): {native.last_error()}")
+        return True
+
+    def local_pointers(self):
+        return self.Ay.data_ptr(), self.By.data_ptr(), self.Az.data_ptr()
+
     def finalize(self) -> np.ndarray:
         m = np.zeros(12)
         self._call(self.L.fftc_slab_finalize, None, None, None, m.ctypes.data)
@@ -154,12 +169,42 @@ def _allreduce(vec: np.ndarray, dist, group, device) -> np.ndarray:
 _STATUS = {0: TerminationStatus.CONVERGED, 1: TerminationStatus.MAX_ITERS, 2: TerminationStatus.DIVERGED}
 
 
-def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend_factory=None, comm=None) -> dict:
+def _gather_pointers(be, dist, group, comm, world):
+    """Every rank's (A_y, B_y, A_z) device pointers, peer-accessible, or None.
+
+    Test communicators gather them directly (one process, one device).  With
+    torch.distributed the buffers would have to live in symmetric memory
+    (torch.distributed._symmetric_memory) to be mapped into every peer; that
+    allocation is not wired into GpuSlab yet, so multi-process runs keep the
+    all-to-all transposes."""
+    if comm is not None and hasattr(comm, "all_gather_object"):
+        return comm.all_gather_object(be.local_pointers())
+    return None
+
+
+def _all_true(flag: bool, dist, group, device, comm) -> bool:
+    if dist is None:
+        return flag
+    v = _allreduce(np.array([0.0 if flag else 1.0]), dist, group, device)
+    return float(v[0]) == 0.0
+
+
+def _barrier(dist, group, comm):
+    if comm is not None and hasattr(comm, "barrier"):
+        comm.barrier()
+    elif dist is not None:
+        dist.barrier(group=group)
+
+
+def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend_factory=None, comm=None,
+               fused: bool = True) -> dict:
     """Slab-decomposed solve of a 3-D cell; every rank returns the same record dict.
 
     `comm` (tests): an object with `rank`, `world`, `all_to_all_single(out,
-    inp, group=None)` and `all_reduce(t, group=None)` standing in for
-    torch.distributed."""
+    inp, group=None)`, `all_reduce(t, group=None)` (and optionally
+    `all_gather_object`, `barrier`) standing in for torch.distributed.
+    `fused`: use the transposes fused into the column passes (peer stores)
+    when every rank can; otherwise the all-to-all transposes."""
     if comm is not None:
         dist, rank, world = comm, comm.rank, comm.world
     else:
@@ -182,15 +227,27 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
             tot = _allreduce(parts[:6], dist, group, device)
             return tot - (world - 1) * e0v
 
+        use_fused = False
+        if fused and world > 1 and hasattr(be, "set_peers"):
+            ptrs = _gather_pointers(be, dist, group, comm, world)
+            ok = ptrs is not None and be.set_peers(world, [p[0] for p in ptrs], [p[1] for p in ptrs],
+                                                    [p[2] for p in ptrs])
+            use_fused = _all_true(ok, dist, group, device, comm)
+            if ok and not use_fused:
+                raise BackendError("ranks disagree on fused transposes")  # cannot undo set_peers on this rank
         be.set_delta(global_delta(be.phase(PH_INIT)))
         history, rec = [], None
         for k in range(1, cfg.max_iters + 1):
             fwd = be.phase(PH_ROWS_FWD)
-            _transpose_z_to_y(be.Az, be.Ay, world, group, dist)
-            if be.em_type:
-                _transpose_z_to_y(be.Bz, be.By, world, group, dist)
+            if use_fused:
+                _barrier(dist, group, comm)  # every y-slab filled by the peers' y passes
+            else:
+                _transpose_z_to_y(be.Az, be.Ay, world, group, dist)
+                if be.em_type:
+                    _transpose_z_to_y(be.Bz, be.By, world, group, dist)
             mid = be.phase(PH_MID)
-            _transpose_y_to_z(be.Ay, be.Az, world, group, dist)
+            if not use_fused:
+                _transpose_y_to_z(be.Ay, be.Az, world, group, dist)
             tot = _allreduce(np.concatenate([fwd[:7], mid[:1]]), dist, group, device)
             rec = be.monitor(tot)
             if int(rec[3]) > len(history):
@@ -201,7 +258,7 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
         means = _allreduce(be.finalize(), dist, group, device)
         sstar = history[-1][0] if history else complex(rec[4], rec[5])
         return dict(status=_STATUS[int(rec[1])], degenerate_flux=bool(rec[2]), iterations=len(history),
-                    sigma_star=sstar, history=history,
+                    sigma_star=sstar, history=history, fused=use_fused,
                     mean_E=np.array([complex(means[2 * c], means[2 * c + 1]) for c in range(3)]),
                     mean_J=np.array([complex(means[6 + 2 * c], means[6 + 2 * c + 1]) for c in range(3)]),
                     world=world)

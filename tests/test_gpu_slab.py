@@ -93,6 +93,17 @@ class ThreadComm:
         t.copy_(tot)
         self._sync()
 
+    def barrier(self):
+        self._sync()
+        self.s.barrier.wait()
+
+    def all_gather_object(self, obj):
+        self.s.buf[self.rank] = obj
+        self.s.barrier.wait()
+        out = list(self.s.buf)
+        self.s.barrier.wait()
+        return out
+
     def all_to_all_single(self, out, inp, group=None):
         import torch
 
@@ -104,7 +115,7 @@ class ThreadComm:
         self.s.barrier.wait()
 
 
-def _run_threads(chi, cfg, world):
+def _run_threads(chi, cfg, world, fused=True):
     import threading
 
     import torch
@@ -117,7 +128,7 @@ def _run_threads(chi, cfg, world):
         try:
             torch.cuda.set_device(0)
             with torch.cuda.stream(torch.cuda.Stream()):
-                out[r] = solve_slab(chi, cfg, comm=ThreadComm(shared, r, world))
+                out[r] = solve_slab(chi, cfg, comm=ThreadComm(shared, r, world), fused=fused)
         except BaseException as e:  # noqa: BLE001 -- reported below
             errs.append(e)
             shared.barrier.abort()
@@ -131,9 +142,10 @@ def _run_threads(chi, cfg, world):
     return out
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["alltoall", "fused"])
 @pytest.mark.parametrize("shape, scheme, world", [((256, 256, 8), "em_sub", 2), ((256, 256, 8), "basic", 4),
-                                                  ((512, 256, 4), "em", 2), ((64, 64, 64), "basic_sub", 4)])
-def test_slab_threads_match_monolithic(shape, scheme, world):
+                                                  ((512, 256, 8), "em", 2), ((64, 64, 64), "basic_sub", 4)])
+def test_slab_threads_match_monolithic(shape, scheme, world, fused):
     """z-slab decomposition at world 2 / 4 on the GPU kernels (rank-local
     slabs with y0/z0 offsets, TMA tile column passes where the line lengths
     allow) against the single-GPU solve: identical iteration counts and
@@ -146,7 +158,13 @@ def test_slab_threads_match_monolithic(shape, scheme, world):
     cfg = fb.SolverConfig(scheme=sk, sigma1=20.0 + 1j, tol=1e-9, max_iters=300, e0=(0.0, 0.6, 0.8),
                           interval=fb.SpectralInterval(ALPHA, BETA) if sk.substituted else None)
     mono = fb.solve(fb.PhaseMap(chi), cfg)
-    recs = _run_threads(chi, cfg, world)
+    recs = _run_threads(chi, cfg, world, fused)
+    # fused transposes need the TMA tile passes: y and z lines of 256..1024 and
+    # nx a multiple of their tile widths; the 64^3 case keeps the all-to-alls
+    def tile_ok(n):
+        return 256 <= n <= 1024 and shape[2] % (8 if n <= 256 else 4 if n <= 512 else 2) == 0
+
+    assert all(r["fused"] == (fused and tile_ok(shape[0]) and tile_ok(shape[1])) for r in recs)
     for r in recs:
         assert r["world"] == world and r["iterations"] == mono.iterations
         assert r["status"] == mono.status
