@@ -133,6 +133,17 @@ void fftc_slab_destroy(fftc_slab* slab);
 int fftc_slab_set_peers(fftc_slab* slab, int32_t world, void* const* Ay, void* const* By, void* const* Az,
                         void* stream);
 
+/* Device buffers shared between rank processes (CUDA IPC), for the fused
+ * transposes when ranks live in different processes: allocate the slab work
+ * buffers here, export their handles (64 bytes each), open the peers'
+ * handles (mapped over NVLink between GPUs, or aliased on one GPU), and pass
+ * the resulting pointers to fftc_slab_set_peers. */
+int fftc_ipc_alloc(int64_t bytes, void** ptr);
+int fftc_ipc_free(void* ptr);
+int fftc_ipc_handle(void* ptr, void* handle64);
+int fftc_ipc_open(const void* handle64, void** ptr);
+int fftc_ipc_close(void* ptr);
+
 /* Same contract, host-resident chi and outputs (the library copies in and
  * out; E/J/aug host buffers are nullable).  For FFI users without a device
  * allocator. */

@@ -1443,6 +1443,49 @@ int fftc_slab_set_peers(fftc_slab* sl, int32_t world, void* const* Ay, void* con
   return 0;
 }
 
+int fftc_ipc_alloc(int64_t bytes, void** ptr) {
+  g_err.clear();
+  if (!ptr || bytes <= 0) {
+    g_err = "ipc alloc: bad argument";
+    return 2;
+  }
+  CK(cudaMalloc(ptr, (size_t)bytes));  // a whole allocation: its IPC handle maps exactly this buffer
+  return 0;
+}
+int fftc_ipc_free(void* ptr) {
+  g_err.clear();
+  CK(cudaFree(ptr));
+  return 0;
+}
+int fftc_ipc_handle(void* ptr, void* handle64) {
+  g_err.clear();
+  if (!ptr || !handle64) {
+    g_err = "ipc handle: null argument";
+    return 2;
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ptr));
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(handle64, &h, sizeof(h));
+  return 0;
+}
+int fftc_ipc_open(const void* handle64, void** ptr) {
+  g_err.clear();
+  if (!handle64 || !ptr) {
+    g_err = "ipc open: null argument";
+    return 2;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+int fftc_ipc_close(void* ptr) {
+  g_err.clear();
+  CK(cudaIpcCloseMemHandle(ptr));
+  return 0;
+}
+
 void fftc_slab_destroy(fftc_slab* sl) {
   if (!sl) return;
   cudaDeviceSynchronize();

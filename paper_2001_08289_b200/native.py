@@ -31,6 +31,11 @@ EXPORTS = (
     "fftc_apply_sigma",
     "fftc_reduce",
     "fftc_slab_set_peers",
+    "fftc_ipc_alloc",
+    "fftc_ipc_free",
+    "fftc_ipc_handle",
+    "fftc_ipc_open",
+    "fftc_ipc_close",
     "fftc_profile",
     "fftc_kernel_stats",
     "fftc_solve_batch",
@@ -114,6 +119,16 @@ def lib():
         L.fftc_slab_finalize.restype = C.c_int
         L.fftc_slab_set_peers.argtypes = [vp, C.c_int32, vp, vp, vp, vp]
         L.fftc_slab_set_peers.restype = C.c_int
+        L.fftc_ipc_alloc.argtypes = [i64, C.POINTER(C.c_void_p)]
+        L.fftc_ipc_alloc.restype = C.c_int
+        L.fftc_ipc_free.argtypes = [vp]
+        L.fftc_ipc_free.restype = C.c_int
+        L.fftc_ipc_handle.argtypes = [vp, vp]
+        L.fftc_ipc_handle.restype = C.c_int
+        L.fftc_ipc_open.argtypes = [vp, C.POINTER(C.c_void_p)]
+        L.fftc_ipc_open.restype = C.c_int
+        L.fftc_ipc_close.argtypes = [vp]
+        L.fftc_ipc_close.restype = C.c_int
         L.fftc_slab_destroy.argtypes = [vp]
         L.fftc_slab_destroy.restype = None
         L.fftc_fft.argtypes = [C.POINTER(Problem), vp, C.c_int32, C.c_int32, vp]

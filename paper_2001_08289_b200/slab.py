@@ -48,21 +48,37 @@ def slab_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     return rank * m, m
 
 
-class GpuSlab:
-    """Per-rank device state behind fftc_slab_* (one rank per GPU)."""
+class _DeviceArray:
+    """A library (CUDA IPC-capable) allocation seen by torch through
+    __cuda_array_interface__ (zero copy)."""
 
-    def __init__(self, chi_local: np.ndarray, n_global, z0, nzl, y0, nyl, cfg: SolverConfig):
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<c16", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class GpuSlab:
+    """Per-rank device state behind fftc_slab_* (one rank per GPU).
+
+    shared=True allocates the slab work buffers through fftc_ipc_alloc, so
+    ranks in other processes can map them (fused transposes)."""
+
+    def __init__(self, chi_local: np.ndarray, n_global, z0, nzl, y0, nyl, cfg: SolverConfig, shared: bool = False):
         import torch
 
         nz, ny, nx = n_global
         self.torch = torch
+        self.L = native.lib()
         self.em_type = cfg.scheme.accelerated
+        self._owned, self._opened = [], []
         self.chi = torch.from_numpy(np.ascontiguousarray(chi_local).astype(np.uint8)).cuda()
         shape_z, shape_y = (3, nzl, ny, nx), (3, nyl, nz, nx)
-        self.Az = torch.empty(shape_z, dtype=torch.complex128, device="cuda")
-        self.Ay = torch.empty(shape_y, dtype=torch.complex128, device="cuda")
-        self.Bz = torch.empty(shape_z, dtype=torch.complex128, device="cuda") if self.em_type else self.Az
-        self.By = torch.empty(shape_y, dtype=torch.complex128, device="cuda") if self.em_type else self.Ay
+        alloc = self._alloc_shared if shared else (
+            lambda shape: torch.empty(shape, dtype=torch.complex128, device="cuda"))
+        self.Az = alloc(shape_z)
+        self.Ay = alloc(shape_y)
+        self.Bz = alloc(shape_z) if self.em_type else self.Az
+        self.By = alloc(shape_y) if self.em_type else self.Ay
         d = native.SlabDesc()
         d.d = 3
         d.n[0], d.n[1], d.n[2] = nx, ny, nz
@@ -70,7 +86,6 @@ class GpuSlab:
         d.chi = self.chi.data_ptr()
         self.params = _params(cfg, 3)
         self.h = C.c_void_p()
-        self.L = native.lib()
         rc = self.L.fftc_slab_create(C.byref(d), C.byref(self.params), self.Az.data_ptr(), self.Bz.data_ptr(),
                                      self.Ay.data_ptr(), self.By.data_ptr(), C.byref(self.h), self._stream())
         if rc:
@@ -114,6 +129,42 @@ class GpuSlab:
     def local_pointers(self):
         return self.Ay.data_ptr(), self.By.data_ptr(), self.Az.data_ptr()
 
+    def _alloc_shared(self, shape):
+        ptr = C.c_void_p()
+        nbytes = int(np.prod(shape)) * 16
+        rc = self.L.fftc_ipc_alloc(nbytes, C.byref(ptr))
+        if rc:
+            raise BackendError(f"fftc_ipc_alloc failed ({rc}): {native.last_error()}")
+        self._owned.append(ptr.value)
+        return self.torch.as_tensor(_DeviceArray(ptr.value, shape), device="cuda")
+
+    def ipc_handles(self):
+        """64-byte CUDA IPC handles of (A_y, B_y, A_z), or None without shared buffers."""
+        if not self._owned:
+            return None
+        out = []
+        for t in (self.Ay, self.By, self.Az):
+            h = C.create_string_buffer(64)
+            rc = self.L.fftc_ipc_handle(t.data_ptr(), h)
+            if rc:
+                raise BackendError(f"fftc_ipc_handle failed ({rc}): {native.last_error()}")
+            out.append(h.raw)
+        return out
+
+    def open_peer(self, handles):
+        """Map another process's (A_y, B_y, A_z); returns their device pointers."""
+        ptrs, seen = [], {}
+        for h in handles:
+            if h not in seen:  # B_y is A_y for basic-type schemes
+                p = C.c_void_p()
+                rc = self.L.fftc_ipc_open(h, C.byref(p))
+                if rc:
+                    raise BackendError(f"fftc_ipc_open failed ({rc}): {native.last_error()}")
+                self._opened.append(p.value)
+                seen[h] = p.value
+            ptrs.append(seen[h])
+        return tuple(ptrs)
+
     def finalize(self) -> np.ndarray:
         m = np.zeros(12)
         self._call(self.L.fftc_slab_finalize, None, None, None, m.ctypes.data)
@@ -123,6 +174,14 @@ class GpuSlab:
         if self.h:
             self.L.fftc_slab_destroy(self.h)
             self.h = C.c_void_p()
+        self.torch.cuda.synchronize()
+        for p in self._opened:
+            self.L.fftc_ipc_close(p)
+        self._opened = []
+        self.Az = self.Ay = self.Bz = self.By = None
+        for p in self._owned:
+            self.L.fftc_ipc_free(p)
+        self._owned = []
 
 
 def _transpose_z_to_y(Az, Ay, world, group, dist):
@@ -161,6 +220,8 @@ def _allreduce(vec: np.ndarray, dist, group, device) -> np.ndarray:
         return vec
     import torch
 
+    if hasattr(dist, "get_backend") and dist.get_backend(group) == "gloo":
+        device = "cpu"  # gloo reduces host tensors
     t = torch.from_numpy(np.ascontiguousarray(vec, dtype=np.float64)).to(device)
     dist.all_reduce(t, group=group)
     return t.cpu().numpy()
@@ -169,17 +230,21 @@ def _allreduce(vec: np.ndarray, dist, group, device) -> np.ndarray:
 _STATUS = {0: TerminationStatus.CONVERGED, 1: TerminationStatus.MAX_ITERS, 2: TerminationStatus.DIVERGED}
 
 
-def _gather_pointers(be, dist, group, comm, world):
+def _gather_pointers(be, dist, group, comm, world, rank):
     """Every rank's (A_y, B_y, A_z) device pointers, peer-accessible, or None.
 
-    Test communicators gather them directly (one process, one device).  With
-    torch.distributed the buffers would have to live in symmetric memory
-    (torch.distributed._symmetric_memory) to be mapped into every peer; that
-    allocation is not wired into GpuSlab yet, so multi-process runs keep the
-    all-to-all transposes."""
+    Threads of one process (test communicators) gather the pointers directly.
+    Processes exchange CUDA IPC handles of their library-allocated slab
+    buffers and map the peers' (NVLink peer mappings between GPUs)."""
     if comm is not None and hasattr(comm, "all_gather_object"):
         return comm.all_gather_object(be.local_pointers())
-    return None
+    if dist is None or not hasattr(be, "ipc_handles"):
+        return None
+    allh = [None] * world
+    dist.all_gather_object(allh, be.ipc_handles(), group=group)
+    if any(h is None for h in allh):
+        return None
+    return [be.local_pointers() if q == rank else be.open_peer(h) for q, h in enumerate(allh)]
 
 
 def _all_true(flag: bool, dist, group, device, comm) -> bool:
@@ -216,7 +281,11 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
     z0, nzl = slab_bounds(nz, rank, world)
     y0, nyl = slab_bounds(ny, rank, world)
     factory = backend_factory or GpuSlab
-    be = factory(chi_global[z0:z0 + nzl], (nz, ny, nx), z0, nzl, y0, nyl, cfg)
+    if factory is GpuSlab:  # processes share their slab buffers for the fused transposes
+        be = GpuSlab(chi_global[z0:z0 + nzl], (nz, ny, nx), z0, nzl, y0, nyl, cfg,
+                     shared=fused and world > 1 and comm is None)
+    else:
+        be = factory(chi_global[z0:z0 + nzl], (nz, ny, nx), z0, nzl, y0, nyl, cfg)
     device = "cuda" if factory is GpuSlab else "cpu"
     if world == 1:
         dist = None
@@ -229,7 +298,7 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
 
         use_fused = False
         if fused and world > 1 and hasattr(be, "set_peers"):
-            ptrs = _gather_pointers(be, dist, group, comm, world)
+            ptrs = _gather_pointers(be, dist, group, comm, world, rank)
             ok = ptrs is not None and be.set_peers(world, [p[0] for p in ptrs], [p[1] for p in ptrs],
                                                     [p[2] for p in ptrs])
             use_fused = _all_true(ok, dist, group, device, comm)
