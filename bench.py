@@ -47,6 +47,8 @@ WORKLOADS = {
     "c2-emsub10": [("em_sub", 10.0)],
     "c2-fast": [("em", 0.1), ("em", 10.0), ("em_sub", 0.1), ("em_sub", 10.0)],
     "c5": None,  # BASELINE configs[4]: 256-point complex sigma1 sweep, em_sub, 1024^2 (see run_c5)
+    "c3": None,  # BASELINE configs[2]: 512^3 centred cube, em_sub, sigma1=100 (see run_3d)
+    "c4": None,  # BASELINE configs[3]: 1024^3 random medium, basic, sigma1=50; z-slabs over N GPUs (run_3d)
 }
 
 
@@ -167,15 +169,29 @@ def _dist():
 # ---------------------------------------------------------------------------
 
 def _oracle_sample(args):
-    scheme, s1, n, iters = args
+    scheme, s1, n, iters = args[:4]
+    geom = args[4] if len(args) > 4 else "square"
     import numpy as np
     from oracle import fftcond_oracle as O
 
-    chi = O.centred_box(n, int(round(SIDE * n)))
+    e0 = None
+    if geom == "square":
+        chi = O.centred_box(n, int(round(SIDE * n)))
+    elif geom == "cube":  # C3 recipe at a bounded size
+        chi = O.centred_box(n, 2 * int(round(0.63 * n / 2)), 3)
+        e0 = (1.0, 0.0, 0.0)
+    else:  # C4 recipe (random medium) at a bounded size
+        rng = np.random.default_rng(20260809)
+        u = rng.random((n,) * 3)
+        k = np.fft.fftfreq(n)
+        k2 = k[:, None, None] ** 2 + k[None, :, None] ** 2 + k[None, None, :] ** 2
+        sm = np.fft.ifftn(np.fft.fftn(u) * np.exp(-2.0 * np.pi ** 2 * 16.0 * k2)).real
+        chi = sm <= np.quantile(sm, 0.30)
+        e0 = (3 ** -0.5,) * 3
     t0 = time.perf_counter()
-    r = O.solve(chi, scheme, s1, tol=1e-300, max_iters=iters, alpha=ALPHA, beta=BETA)
+    r = O.solve(chi, scheme, s1, e0=e0, tol=1e-300, max_iters=iters, alpha=ALPHA, beta=BETA)
     dt = time.perf_counter() - t0
-    return n * n * r.iterations, dt
+    return int(chi.size) * r.iterations, dt
 
 
 def cpu_baseline(iters: int = 6) -> dict:
@@ -197,14 +213,25 @@ def run_reference(a):
         return 0
     from concurrent.futures import ProcessPoolExecutor
 
-    solves = WORKLOADS[a.workload]
     ncpu = os.cpu_count() or 1
     # every host core gets a bounded sample of one of the workload's solves
     # (cycling through them); the reference is single threaded, so this is
     # the throughput the host can deliver
     procs = max(1, ncpu)
     iters = a.ref_iters
-    jobs = [(solves[i % len(solves)][0], solves[i % len(solves)][1], N_GRID, iters) for i in range(max(procs, len(solves)))]
+    if a.workload == "c3":  # bounded 3-D samples: the reference itself is 2-D only (restatement, 128^3)
+        solves, tasks = [("em_sub", 100.0)], [("em_sub", 100.0, 128, iters, "cube")]
+    elif a.workload == "c4":
+        solves, tasks = [("basic", 50.0)], [("basic", 50.0, 128, iters, "random")]
+    elif a.workload == "c5":
+        from paper_2001_08289_b200.sweep import c5_points
+
+        pts = c5_points(max(procs, 8))
+        solves, tasks = [("em_sub", p) for p in pts], [("em_sub", p, 1024, iters) for p in pts]
+    else:
+        solves = WORKLOADS[a.workload]
+        tasks = [(sch, v, N_GRID, iters) for sch, v in solves]
+    jobs = [tasks[i % len(tasks)] for i in range(max(procs, len(tasks)))]
     times, vox = [], 0
     with ProcessPoolExecutor(max_workers=procs) as ex:
         for step in range(a.warmup + a.steps):
@@ -221,7 +248,8 @@ def run_reference(a):
         "value": value, "unit": "voxel-iterations/s", "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 (complex128)", "data": "synthetic (reference square-array builder)",
-        "config": _config(a),
+        "config": _config(a) if WORKLOADS[a.workload] else {"workload": a.workload, "sample_grid": jobs[0][2],
+                                                            "note": "bounded samples of the workload's solves"},
         "cpu_baseline": {"value": value, "unit": "voxel-iterations/s", "cores": procs, "kind": "port",
                          "sample": f"{len(jobs)} bounded samples ({iters} iterations each) cycling through the "
                                    f"{len(solves)} solves, {procs} processes on {ncpu} host CPUs; oracle/fftcond_oracle.py "
@@ -482,6 +510,105 @@ def run_c5(a):
     return 0
 
 
+def run_3d(a):
+    """BASELINE configs[2] (C3: 512^3 cube, em_sub, sigma1 = 100, e0 = x) and
+    configs[3] (C4: 1024^3 seeded random medium, f = 0.30, basic, sigma1 = 50,
+    e0 = (1,1,1)/sqrt 3), tol 1e-8.  One step = one whole solve through the
+    public API (host phase map in, history out).  C4 on N > 1 GPUs runs the
+    z-slab decomposition with the transposes fused into the column passes
+    (CUDA IPC peer buffers); time = max over ranks (strong scaling)."""
+    import numpy as np
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2001_08289_b200 as fb
+    from paper_2001_08289_b200 import native
+    from paper_2001_08289_b200.slab import solve_slab
+
+    iv = fb.SpectralInterval(ALPHA, BETA)
+    if a.workload == "c3":
+        n = a.n3d or 512
+        if ws > 1:
+            raise SystemExit("c3 is a single-GPU configuration (BASELINE configs[2])")
+        pm = fb.build_cube_array(n, 2 * int(round(0.63 * n / 2)))
+        cfg = fb.SolverConfig(scheme=fb.SchemeKind.EYRE_MILTON_SUB, sigma1=100.0, tol=1e-8, max_iters=20000,
+                              e0=(1.0, 0.0, 0.0), interval=iv)
+        work = f"BASELINE configs[2]: {n}^3 centred cube side {2 * int(round(0.63 * n / 2))}, em_sub, sigma1=100, tol 1e-8"
+        bpv = 15 * 48 + 6 * float(pm.volume_fraction) * 48 + 2
+    else:
+        n = a.n3d or 1024
+        pm = fb.build_random_medium(n, 3, seed=20260809, smoothing=4.0, fraction=0.30)
+        cfg = fb.SolverConfig(scheme=fb.SchemeKind.BASIC, sigma1=50.0, tol=1e-8, max_iters=20000,
+                              e0=(1 / 3 ** 0.5,) * 3)
+        work = (f"BASELINE configs[3]: {n}^3 random medium (seed 20260809, smoothing 4, f 0.30), basic, "
+                f"sigma1=50, tol 1e-8")
+        bpv = 11 * 48 + 2
+
+    def one(c):
+        if ws > 1:
+            return solve_slab(pm.chi, c, fused=True)
+        r = fb.solve(pm, c)
+        return {"iterations": r.iterations, "status": r.status, "sigma_star": r.sigma_star, "fused": False}
+
+    warm = fb.SolverConfig(scheme=cfg.scheme, sigma1=cfg.sigma1, tol=1e-300, max_iters=3, e0=cfg.e0,
+                           interval=cfg.interval)
+    for _ in range(max(1, a.warmup)):
+        one(warm)
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = native.lib().fftc_launch_count()
+    times, rec = [], None
+    for _ in range(a.steps):
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rec = one(cfg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    clk = clocks.stop()
+    launches = native.lib().fftc_launch_count() - launches0
+    ms = sum(times) / len(times)
+    if ws > 1:
+        t = torch.tensor([ms, float(launches)], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
+        ms, launches = float(t[0]), int(t[1])
+    vox = n ** 3 * rec["iterations"]
+    value = vox / (ms / 1e3)
+    hbm, src = _peaks()
+    line = {"metric": "fp64 voxel-iterations/sec of the FFT iteration", "value": value,
+            "unit": "voxel-iterations/s", "n_gpus": ws, "steps": len(times), "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128)",
+            "data": "synthetic (seeded reference-style builders)",
+            "config": {"workload": work, "grid": [n, n, n],
+                       "parallelism": f"z-slabs over {ws} GPUs, transposes fused into the column passes"
+                       if ws > 1 else "single GPU",
+                       "l2": "fields of 6-48 GiB >> 126 MB L2"},
+            "iteration_roofline": {"bytes_per_voxel_iter_survey": bpv, "achieved_gbs": value * bpv / 1e9 / ws,
+                                   "frac": value * bpv / 1e9 / hbm / ws, "peak_gbs": hbm, "peak_source": src},
+            "e2e": {"value": value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": n ** 3,
+                    "d2h_bytes_per_step": 24 * rec["iterations"],
+                    "note": "each step is one solve through the public API: host phase map in, history out"},
+            "gpu_launches": int(launches), "clocks": clk, "iterations": rec["iterations"],
+            "status": rec["status"].value, "sigma_star": [rec["sigma_star"].real, rec["sigma_star"].imag],
+            "fused_transposes": bool(rec.get("fused", False))}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -493,9 +620,12 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=6, help="iterations per solve in cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c5-points", type=int, default=256)
+    ap.add_argument("--n3d", type=int, default=0, help="c3/c4 grid side (default: the BASELINE size)")
     a = ap.parse_args()
     if a.workload == "c5" and a.impl == "ours":
         return run_c5(a)
+    if a.workload in ("c3", "c4") and a.impl == "ours":
+        return run_3d(a)
     if a.impl == "reference":
         return run_reference(a)
     return run_ours(a)
