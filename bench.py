@@ -552,7 +552,7 @@ def run_3d(a):
     def one(c):
         if ws > 1:
             return solve_slab(pm.chi, c, fused=True)
-        r = fb.solve(pm, c)
+        r = fb.solve(pm, c, fields=False)  # no E/J output fields: 96 GB at 1024^3
         return {"iterations": r.iterations, "status": r.status, "sigma_star": r.sigma_star, "fused": False}
 
     warm = fb.SolverConfig(scheme=cfg.scheme, sigma1=cfg.sigma1, tol=1e-300, max_iters=3, e0=cfg.e0,

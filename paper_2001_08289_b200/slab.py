@@ -287,7 +287,7 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
     else:
         be = factory(chi_global[z0:z0 + nzl], (nz, ny, nx), z0, nzl, y0, nyl, cfg)
     device = "cuda" if factory is GpuSlab else "cpu"
-    if world == 1:
+    if world == 1 and comm is None:
         dist = None
     e0 = cfg.e0_vector(3)
     e0v = np.array([[z.real, z.imag] for z in e0]).ravel()
@@ -297,7 +297,7 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
             return tot - (world - 1) * e0v
 
         use_fused = False
-        if fused and world > 1 and hasattr(be, "set_peers"):
+        if fused and (world > 1 or comm is not None) and hasattr(be, "set_peers"):
             ptrs = _gather_pointers(be, dist, group, comm, world, rank)
             ok = ptrs is not None and be.set_peers(world, [p[0] for p in ptrs], [p[1] for p in ptrs],
                                                     [p[2] for p in ptrs])

@@ -332,28 +332,28 @@ def _check_scheme(cfg: SolverConfig, expected: SchemeKind):
         raise ContractError(f"config carries scheme {cfg.scheme.value!r}, expected {expected.value!r}")
 
 
-def solve_basic(pmap: PhaseMap, cfg: SolverConfig) -> SolveResult:
+def solve_basic(pmap: PhaseMap, cfg: SolverConfig, *, fields: bool = True) -> SolveResult:
     """Moulinec-Suquet basic scheme, sigma0 = (sigma1 + 1)/2."""
     _check_scheme(cfg, SchemeKind.BASIC)
-    return _solve_h(pmap, cfg, accelerated=False)
+    return _solve_h(pmap, cfg, accelerated=False, want_fields=fields)
 
 
-def solve_em(pmap: PhaseMap, cfg: SolverConfig) -> SolveResult:
+def solve_em(pmap: PhaseMap, cfg: SolverConfig, *, fields: bool = True) -> SolveResult:
     """Eyre-Milton scheme, sigma0 = sqrt(sigma1)."""
     _check_scheme(cfg, SchemeKind.EYRE_MILTON)
-    return _solve_h(pmap, cfg, accelerated=True)
+    return _solve_h(pmap, cfg, accelerated=True, want_fields=fields)
 
 
-def solve_basic_sub(pmap: PhaseMap, cfg: SolverConfig) -> SolveResult:
+def solve_basic_sub(pmap: PhaseMap, cfg: SolverConfig, *, fields: bool = True) -> SolveResult:
     """Basic scheme in the substituted (Q, S, T) space, t = map_t(sigma1)."""
     _check_scheme(cfg, SchemeKind.BASIC_SUB)
-    return _solve_aug(pmap, cfg, accelerated=False)
+    return _solve_aug(pmap, cfg, accelerated=False, want_fields=fields)
 
 
-def solve_em_sub(pmap: PhaseMap, cfg: SolverConfig) -> SolveResult:
+def solve_em_sub(pmap: PhaseMap, cfg: SolverConfig, *, fields: bool = True) -> SolveResult:
     """Eyre-Milton scheme in the substituted space, sigma0 = sqrt(t)."""
     _check_scheme(cfg, SchemeKind.EYRE_MILTON_SUB)
-    return _solve_aug(pmap, cfg, accelerated=True)
+    return _solve_aug(pmap, cfg, accelerated=True, want_fields=fields)
 
 
 _DISPATCH = {
@@ -364,9 +364,13 @@ _DISPATCH = {
 }
 
 
-def solve(pmap: PhaseMap, cfg: SolverConfig) -> SolveResult:
-    """Run the scheme named by ``cfg.scheme``."""
-    return _DISPATCH[cfg.scheme](pmap, cfg)
+def solve(pmap: PhaseMap, cfg: SolverConfig, *, fields: bool = True) -> SolveResult:
+    """Run the scheme named by ``cfg.scheme``.
+
+    ``fields=False`` (extension) skips the E / J / augmented output fields --
+    sigma*, the history and the field means are still returned.  At 1024^3
+    two device fields are 96 GB on top of the ~96 GB iteration workspace."""
+    return _DISPATCH[cfg.scheme](pmap, cfg, fields=fields)
 
 
 def estimate_rate(history: ConvergenceHistory, window: int) -> float:
