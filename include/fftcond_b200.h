@@ -220,6 +220,11 @@ int fftc_version(void);
 /* Total kernels launched by this library in this process. */
 int64_t fftc_launch_count(void);
 
+/* Work-field layout of this thread's last fftc_solve: the z-block shift
+ * (2^shift consecutive z-planes of a y-row adjacent; 0 = the reference
+ * (c, z, y, x) layout).  Diagnostics only; results do not depend on it. */
+int32_t fftc_last_layout(void);
+
 #ifdef __cplusplus
 }
 #endif

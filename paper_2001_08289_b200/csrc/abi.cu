@@ -203,6 +203,47 @@ bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W
   return r == CUDA_SUCCESS;
 }
 
+// 5-D maps over a work field in the z-blocked layout (Args::zbs, ZB = 2^zbs
+// z-planes of a y-row adjacent), box = W x-columns x one whole line x 3
+// components landing as [c][pos][w] like make_line_map:
+//   z lines (axis 2, outer y): {2nx, ZB (zl), nz/ZB (zh), ny, 3}
+//   y lines (axis 1, outer z): {2nx, BY, (ny/BY)*(nz/ZB), ZB (zl), 3} -- the
+//     y-block and zh dimensions fold into one because the zh step is exactly
+//     ny/BY y-blocks; outer z sits at {(z >> zbs) * ny/BY, z & (ZB-1)}.
+bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long long nz, int W, int axis, int zbs) {
+  EncodeTiledFn enc = encode_tiled();
+  const long long ZB = 1LL << zbs, N = nx * ny * nz;
+  if (!enc || nx % W || nz % ZB) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5];
+  if (axis == 2) {
+    if (ZB > 256 || nz / ZB > 256) return false;
+    const cuuint64_t d5[5] = {(cuuint64_t)(2 * nx), (cuuint64_t)ZB, (cuuint64_t)(nz / ZB), (cuuint64_t)ny, 3};
+    const cuuint64_t s4[4] = {(cuuint64_t)(nx * 16), (cuuint64_t)(ny * ZB * nx * 16), (cuuint64_t)(ZB * nx * 16),
+                              (cuuint64_t)(N * 16)};
+    const cuuint32_t b5[5] = {(cuuint32_t)(2 * W), (cuuint32_t)ZB, (cuuint32_t)(nz / ZB), 1, 3};
+    memcpy(dims, d5, sizeof(dims));
+    memcpy(strides, s4, sizeof(strides));
+    memcpy(box, b5, sizeof(box));
+  } else {
+    const long long BY = ny < 256 ? ny : 256;
+    if (ny % BY) return false;
+    const cuuint64_t d5[5] = {(cuuint64_t)(2 * nx), (cuuint64_t)BY, (cuuint64_t)((ny / BY) * (nz / ZB)), (cuuint64_t)ZB,
+                              3};
+    const cuuint64_t s4[4] = {(cuuint64_t)(ZB * nx * 16), (cuuint64_t)(BY * ZB * nx * 16), (cuuint64_t)(nx * 16),
+                              (cuuint64_t)(N * 16)};
+    const cuuint32_t b5[5] = {(cuuint32_t)(2 * W), (cuuint32_t)BY, (cuuint32_t)(ny / BY), 1, 3};
+    memcpy(dims, d5, sizeof(dims));
+    memcpy(strides, s4, sizeof(strides));
+    memcpy(box, b5, sizeof(box));
+  }
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("FFTC_VERBOSE")) fprintf(stderr, "[fftc] z-blocked tensor map failed: %d\n", (int)r);
+  return r == CUDA_SUCCESS;
+}
+
 // one TMA 3-D column pass: tiles of W x-columns x `nouter` outer lines,
 // fields A (and B when given), all three components per tile
 struct Col3Pass {
@@ -215,6 +256,7 @@ struct Col3Pass {
 bool col3_pass(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B, long long L, long long line_stride,
                long long nouter, long long outer_stride, long long comp_stride, int nfields, int axis, int o0, int on) {
   p.ok = false;
+  p.g = Line3{};
   const char* sel = getenv("FFTC_TMA_COLS3");  // "0": the strip kernels (k_col), for comparison
   if (!k.fn || k.max_active <= 0 || (sel && atoi(sel) == 0)) return false;
   const int W = col3_tile_w(L);
@@ -229,6 +271,46 @@ bool col3_pass(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B, lon
   p.tiles = nouter * (a.nx / W) * nfields;
   p.ok = true;
   return true;
+}
+
+// the same pass over work fields in the z-blocked layout (monolithic 3-D solve)
+bool col3_pass_zblk(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B, int axis, int zbs, int nfields) {
+  p.ok = false;
+  p.g = Line3{};
+  const char* sel = getenv("FFTC_TMA_COLS3");
+  if (!k.fn || k.max_active <= 0 || (sel && atoi(sel) == 0)) return false;
+  const long long nx = a.nx, ny = a.ny, nz = a.nz;
+  const long long L = axis == 2 ? nz : ny;
+  const int W = col3_tile_w(L);
+  if (!make_zblk_map(&p.mA, A, nx, ny, nz, W, axis, zbs)) return false;
+  if (!make_zblk_map(&p.mB, B ? B : A, nx, ny, nz, W, axis, zbs)) return false;
+  p.k = &k;
+  p.g.nouter = (int)(axis == 2 ? ny : nz);
+  p.g.o0 = 0;
+  p.g.on = (int)(axis == 2 ? ny : nz);
+  p.g.nfields = nfields;
+  p.g.axis = axis;
+  p.g.obs = axis == 1 ? zbs : 0;
+  p.g.om = axis == 1 ? (int)(ny / (ny < 256 ? ny : 256)) : 0;
+  p.tiles = (long long)p.g.nouter * (nx / W) * nfields;
+  p.ok = true;
+  return true;
+}
+
+// z-block shift for the monolithic 3-D solve's work fields.  A y-line then
+// spans ny*ZB*nx*16 B and a z-line nz/ZB blocks, one 2 MB page each; ZB
+// balances the two page counts (ZB^2 = nz * 2^17 / (nx*ny)): 16 at 512^3 and
+// 1024^3.  Measured at 1024^3 basic (scripts/kernels_3d.py): ZB = 1 (the
+// reference layout) 174 ms/iteration, z pass 94 ms; ZB = 8/16/32/64 142 /
+// 130 / 140 / 146 ms.  FFTC_ZBLOCK=<shift> overrides, 0 keeps the reference
+// layout.
+thread_local int g_last_zbs = 0;
+int zblock_shift(long long nx, long long ny, long long nz) {
+  int s = (int)std::floor(0.5 * std::log2((double)nz * 131072.0 / ((double)nx * (double)ny)) + 0.5);
+  s = std::max(1, std::min(s, 6));
+  if (const char* e = getenv("FFTC_ZBLOCK")) s = atoi(e);
+  while (s > 0 && (1LL << s) > nz) --s;
+  return s < 0 ? 0 : s;
 }
 
 double2 C2(const double* p) { return make_double2(p[0], p[1]); }
@@ -430,6 +512,7 @@ extern "C" {
 const char* fftc_last_error(void) { return g_err.c_str(); }
 int fftc_version(void) { return 100; }
 int64_t fftc_launch_count(void) { return g_launches.load(); }
+int32_t fftc_last_layout(void) { return g_last_zbs; }
 int fftc_supported_length(int64_t n) { return lg2_exact(n) > 0 ? 1 : 0; }
 
 void fftc_profile(int32_t enable) {
@@ -600,12 +683,23 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     // 3-D TMA column passes (cols3_tma.cuh) where the line lengths allow
     Col3Pass zmid, yfwd, yinv;
     const PeerOut* no_peer = nullptr;
+    a.zbs = 0;
+    g_last_zbs = 0;
     if (d == 3) {
-      col3_pass(zmid, TZ.col[em_type ? KC_MID3T_EM : KC_MID3T_BASIC], a, a.A, em_type ? a.B : nullptr, nz, nx * ny, ny,
-                nx, N, em_type ? 2 : 1, 2, 0, (int)ny);
-      col3_pass(yfwd, TY.col[KC_FWD3T], a, a.A, em_type ? a.B : nullptr, ny, nx, nz, nx * ny, N, em_type ? 2 : 1, 1, 0,
-                (int)nz);
-      col3_pass(yinv, TY.col[KC_INV3T], a, a.A, nullptr, ny, nx, nz, nx * ny, N, 1, 1, 0, (int)nz);
+      // z-blocked work fields when all three column passes run on TMA tiles
+      const int zbs = zblock_shift(nx, ny, nz);
+      const KInfo& kz = TZ.col[em_type ? KC_MID3T_EM : KC_MID3T_BASIC];
+      if (zbs > 0 && col3_pass_zblk(zmid, kz, a, a.A, em_type ? a.B : nullptr, 2, zbs, em_type ? 2 : 1) &&
+          col3_pass_zblk(yfwd, TY.col[KC_FWD3T], a, a.A, em_type ? a.B : nullptr, 1, zbs, em_type ? 2 : 1) &&
+          col3_pass_zblk(yinv, TY.col[KC_INV3T], a, a.A, nullptr, 1, zbs, 1)) {
+        a.zbs = zbs;
+        g_last_zbs = zbs;
+      } else {
+        col3_pass(zmid, kz, a, a.A, em_type ? a.B : nullptr, nz, nx * ny, ny, nx, N, em_type ? 2 : 1, 2, 0, (int)ny);
+        col3_pass(yfwd, TY.col[KC_FWD3T], a, a.A, em_type ? a.B : nullptr, ny, nx, nz, nx * ny, N, em_type ? 2 : 1, 1,
+                  0, (int)nz);
+        col3_pass(yinv, TY.col[KC_INV3T], a, a.A, nullptr, ny, nx, nz, nx * ny, N, 1, 1, 0, (int)nz);
+      }
     }
     const long long mid_lines = use_tma_mid ? nx * (em_type ? 2 : 1)
                                             : (long long)mid.nouter * mid.nstrips * (em_type ? 2 : 1);

@@ -44,19 +44,23 @@ struct Col3Tma {
   static_assert(SMEM <= 232448 - 512, "shared memory budget");
 };
 
-__device__ __forceinline__ void col3_issue(const CUtensorMap* tm, double2* slot, uint64_t* bar, int x0, int o,
+// tensor-map coordinates (dims 2 and 3) of outer line o (Line3::obs/om)
+__device__ __forceinline__ int2 col3_outer(const Line3& g, int o) {
+  return g.om > 0 ? make_int2((o >> g.obs) * g.om, o & ((1 << g.obs) - 1)) : make_int2(0, o);
+}
+__device__ __forceinline__ void col3_issue(const CUtensorMap* tm, double2* slot, uint64_t* bar, int x0, int2 oc,
                                            unsigned tx) {
   bulk_wait_read0();  // the TMA store that last used this slot has read it out
   mbar_expect_tx(bar, tx);
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
       "%6}], [%7];" ::"r"(smem_u32(slot)),
-      "l"(tm), "r"(2 * x0), "r"(0), "r"(0), "r"(o), "r"(0), "r"(smem_u32(bar))
+      "l"(tm), "r"(2 * x0), "r"(0), "r"(oc.x), "r"(oc.y), "r"(0), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2* slot, int x0, int o) {
+__device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2* slot, int x0, int2 oc) {
   asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(tm),
-               "r"(2 * x0), "r"(0), "r"(0), "r"(o), "r"(0), "r"(smem_u32(slot))
+               "r"(2 * x0), "r"(0), "r"(oc.x), "r"(oc.y), "r"(0), "r"(smem_u32(slot))
                : "memory");
 }
 
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
   if (threadIdx.x == 0 && nmine > 0) {
     int f, o, x0;
     coords(0, f, o, x0);
-    col3_issue(f == 0 ? &tmA : &tmB, smem, &bars[0], x0, o, K::TX);
+    col3_issue(f == 0 ? &tmA : &tmB, smem, &bars[0], x0, col3_outer(g, o), K::TX);
   }
   double2* tws = smem + K::NSLOT * K::SLOT;
   for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[g.axis][i]);
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
       // tile k+1 into the other slot, whose store (tile k-1) was committed one tile ago
       int nf, no, nx0;
       coords(k + 1, nf, no, nx0);
-      col3_issue(nf == 0 ? &tmA : &tmB, smem + (s ^ 1) * K::SLOT, &bars[s ^ 1], nx0, no, K::TX);
+      col3_issue(nf == 0 ? &tmA : &tmB, smem + (s ^ 1) * K::SLOT, &bars[s ^ 1], nx0, col3_outer(g, no), K::TX);
     }
     double2* xb = slot + (comp * W + w) * K::XS;
     const bool parseval_only = (MODE == MID_EM) && f == 1;
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
       fence_proxy_async();
       __syncthreads();
       if (threadIdx.x == 0) {
-        col3_store(f == 0 ? &tmA : &tmB, slot, x0, o);
+        col3_store(f == 0 ? &tmA : &tmB, slot, x0, col3_outer(g, o));
         bulk_commit();
       }
     } else {

@@ -64,7 +64,7 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
     }
   }
   mbar_expect_tx(bar, tx);
-  bulk_g2s(stage, (SW == 1 ? a.X[0] : a.A) + off, (unsigned)(L * sizeof(double2)), bar);
+  bulk_g2s(stage, SW == 1 ? a.X[0] + off : a.A + work_off(a, c, row), (unsigned)(L * sizeof(double2)), bar);
   if constexpr (K::X0_ROW) bulk_g2s(stage + K::LP, a.X[0] + off, (unsigned)(L * sizeof(double2)), bar);
   if constexpr (K::ST_ROWS > 0) {
     if (nb) {
@@ -204,8 +204,9 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
       fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
     }
     if constexpr (SW == 1) {
+      const size_t woff = work_off(a, c, row);  // work field row (z-blocked in 3-D)
 #pragma unroll
-      for (int i = 0; i < E; ++i) OUT[off + pos_last<L, E>(false, t, i)] = v[0][i];
+      for (int i = 0; i < E; ++i) OUT[woff + pos_last<L, E>(false, t, i)] = v[0][i];
     } else {
       // ---- epilogue: state update for iteration k+1 (solvers.py:303-308, :398-411) ----
 #pragma unroll

@@ -78,6 +78,11 @@ struct Args {
   DevState* st;
   unsigned long long* dbg;  // debug phase counters (FFTC_PHASE_TIMING builds), else null
   int dist;                 // slab-decomposed solve: sweeps leave rank-local partials, the host combines
+  // z-blocked layout of the work fields A/B (3-D): row (z, y) of component c
+  // starts at c*N + (((z >> zbs)*ny + y) << zbs | (z & (2^zbs - 1)))*nx, i.e.
+  // 2^zbs consecutive z-planes of one y-row are adjacent, so a z-line touches
+  // nz / 2^zbs 2 MB pages instead of nz.  zbs = 0 is the reference layout.
+  int zbs;
   const double2* tw[3];  // twiddles for n_x, n_y, n_z
   // scalars (host-prepared, see abi.cu)
   double2 sigma1, s0, e0[3];
@@ -94,6 +99,14 @@ struct Args {
   double2 sinv;                    // 1/(1+s0)
   double2 cinv_p1, cinv_p2, cinv_p3;  // ((t-1)/(t+s0)) p_i
 };
+
+// element offset of row `row` = z*ny + y of component c of a work field (A/B)
+__device__ __forceinline__ size_t work_off(const Args& a, int c, long long row) {
+  const int z = (int)(row / a.ny), y = (int)(row - (long long)z * a.ny);
+  const int s = a.zbs;
+  const long long r = ((long long)((z >> s) * a.ny + y) << s) | (z & ((1 << s) - 1));
+  return (size_t)c * a.N + (size_t)r * a.nx;
+}
 
 // ----------------------------------------------------------------------------
 // deterministic block reduction + last-CTA combine
@@ -307,7 +320,7 @@ __device__ __forceinline__ void prefetch_row_inputs(const Args& a, long long ln,
   const size_t off = (size_t)c * a.N + (size_t)row * L;
   constexpr unsigned RB = (unsigned)(L * sizeof(double2));
   l2_prefetch(a.chi + (size_t)row * L, L);
-  if (SWEEP3) l2_prefetch(a.A + off, RB);
+  if (SWEEP3) l2_prefetch(a.A + work_off(a, c, row), RB);
   if (!SWEEP3 || S == BASIC || S == BASIC_SUB) l2_prefetch(a.X[0] + off, RB);
   if (S == BASIC_SUB || S == EM_SUB) {
     const int2 ext = a.row_ext[row];
@@ -364,6 +377,7 @@ __global__ void __launch_bounds__(G * Sweep1Traits<S>::C * (L / E), 2) k_sweep1(
     const size_t off = (size_t)c * a.N + (size_t)row * L;
     const uint8_t* chi = a.chi + (size_t)row * L;
     const double2 dl = a.st->delta[c];
+    const size_t woff = work_off(a, c, row);  // work field A/B row
     if (t == 0 && ch == 0) prefetch_row_inputs<S, L, false>(a, line + (long long)gridDim.x * G, lines, rows);
     double2 v[1][E];
 #pragma unroll
@@ -407,7 +421,7 @@ __global__ void __launch_bounds__(G * Sweep1Traits<S>::C * (L / E), 2) k_sweep1(
     fft_line<L, E, 1, false>(v, t, a.tw[0], buf, SyncAll{});
     if (live) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) OUT[off + pos_last<L, E>(false, t, i)] = v[0][i];
+      for (int i = 0; i < E; ++i) OUT[woff + pos_last<L, E>(false, t, i)] = v[0][i];
     }
   }
   double tot[NQ];
@@ -443,10 +457,11 @@ __global__ void __launch_bounds__(G*(L / E), 2) k_sweep3(Args a) {
     const size_t off = (size_t)c * a.N + (size_t)row * L;
     const uint8_t* chi = a.chi + (size_t)row * L;
     const double2 dl = a.st->delta[c];
+    const size_t woff = work_off(a, c, row);  // work field A/B row
     if (t == 0) prefetch_row_inputs<S, L, true>(a, line + (long long)gridDim.x * G, lines, rows);
     double2 v[1][E];
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[0][i] = live ? a.A[off + pos_first<L, E>(true, t, i)] : czero();
+    for (int i = 0; i < E; ++i) v[0][i] = live ? a.A[woff + pos_first<L, E>(true, t, i)] : czero();
     fft_line<L, E, 1, true>(v, t, a.tw[0], buf, SyncAll{});
     if (!live) continue;
 #pragma unroll
@@ -561,7 +576,10 @@ struct Line3 {
   int o0, on;   // global index of outer 0 and the outer axis extent (wave numbers)
   int nfields;  // 1, or 2 (fields A and B: EM-type schemes)
   int axis;     // twiddle table of the line axis (1 = y, 2 = z)
-  int pad[3];
+  // tensor-map coordinates of outer line o: {.., (o >> obs) * om, o & (2^obs - 1), ..}
+  // when om > 0 (y passes over the z-blocked layout), else {.., 0, o, ..}
+  int obs, om;
+  int pad;
 };
 
 // Destinations of a column pass whose outputs go straight to the rank that

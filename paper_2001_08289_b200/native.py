@@ -25,6 +25,7 @@ EXPORTS = (
     "fftc_last_error",
     "fftc_version",
     "fftc_launch_count",
+    "fftc_last_layout",
     "fftc_fft",
     "fftc_gamma1",
     "fftc_aug_apply",
@@ -151,6 +152,7 @@ def lib():
         L.fftc_last_error.restype = C.c_char_p
         L.fftc_version.restype = C.c_int
         L.fftc_launch_count.restype = C.c_int64
+        L.fftc_last_layout.restype = C.c_int32
         _lib = L
         return L
 
@@ -164,6 +166,11 @@ def kernel_stats() -> dict:
     buf = (KStat * 16)()
     n = lib().fftc_kernel_stats(buf, 16)
     return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(n)}
+
+
+def last_layout() -> int:
+    """z-block shift of this thread's last solve's work fields (0 = reference layout)."""
+    return int(lib().fftc_last_layout())
 
 
 def last_error() -> str:

@@ -171,3 +171,28 @@ def test_3d_tma_column_passes_vs_oracle(shape, scheme):
     for h, (_, s, res) in zip(r.history, ref.history):
         assert abs(h.sigma_star - s) <= 1e-10 * abs(s)
         assert abs(h.residual - res) <= 1e-6 * res
+
+
+@pytest.mark.parametrize("shape, scheme", [((256, 256, 8), "em_sub"), ((512, 256, 8), "basic"),
+                                           ((256, 512, 8), "em"), ((256, 256, 16), "basic_sub")])
+def test_3d_zblocked_work_layout_bit_identical(shape, scheme, monkeypatch):
+    """The z-blocked work-field layout (Args::zbs, 32 z-planes per block) only
+    moves data: histories are bit identical to the reference layout
+    (FFTC_ZBLOCK=0), for several block shifts."""
+    import paper_2001_08289_b200 as fb
+
+    rng = np.random.default_rng(5)
+    pm = fb.PhaseMap(rng.random(shape) < 0.3)
+    sk = fb.SchemeKind(scheme)
+    cfg = fb.SolverConfig(scheme=sk, sigma1=10.0 + 2j, tol=1e-9, max_iters=120, e0=(0.6, 0.0, 0.8),
+                          interval=fb.SpectralInterval(ALPHA, BETA) if sk.substituted else None)
+    from paper_2001_08289_b200 import native
+
+    runs = {}
+    for zb in ("0", "5", "3", "8"):
+        monkeypatch.setenv("FFTC_ZBLOCK", zb)
+        r = fb.solve(pm, cfg)
+        assert native.last_layout() == int(zb)  # the blocked path really ran
+        runs[zb] = [(h.sigma_star, h.residual) for h in r.history]
+    for zb in ("5", "3", "8"):
+        assert runs[zb] == runs["0"], zb
