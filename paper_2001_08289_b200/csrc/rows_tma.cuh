@@ -96,6 +96,39 @@ __device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, int line,
   if (S == EM_SUB) l2_prefetch(a.X[2] + off, nb);
 }
 
+// em_sub sweep 1 with its two channels (Rq: channel 0, Jq: channel 1): thread
+// (ch, t) evaluates the prologue (solvers.py:398-420: A applied to (Q, S, T),
+// the pinned flux) of elements H*E/2 .. H*E/2 + E/2 - 1 for BOTH channels, so
+// apply_A and the S/T loads run once per element instead of once per channel,
+// keeps its own channel's values and stages the partner's (thread (1-ch, t))
+// at the element's position in `other` (channel 0's main row / channel 1's
+// exchange buffer; each position is read and rewritten by one thread only).
+template <int H, int L, int E, int NQ>
+__device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)[1][E], const double2* st,
+                                                     const uint8_t* chi_s, double2* other, int t, int c, size_t off,
+                                                     double2 dl, double (&acc)[NQ]) {
+#pragma unroll
+  for (int k = 0; k < E / 2; ++k) {
+    const int i = H * (E / 2) + k;
+    const int x = pos_first<L, E>(false, t, i);
+    const bool in1 = chi_s[x] != 0;
+    const double2 q = st[x];
+    double2 sv = czero(), tv = czero();
+    if (in1) {
+      sv = a.X[1][off + x];
+      tv = a.X[2][off + x];
+    }
+    const AugFlux f = apply_A(a, in1, q, sv, tv);
+    double2 jq, js;
+    pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
+    acc_c<NQ>(acc, c, jq);
+    if (in1) acc[NQ - 1] += cabs2(js);
+    const double2 rq = csub(f.jq, cmul(a.s0, q));
+    v[0][i] = H == 0 ? rq : jq;
+    other[x] = H == 0 ? jq : rq;
+  }
+}
+
 template <int S, int SW, int L>
 __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowTma<S, SW, L>::ST_ROWS ? 1 : 2)) k_rows_tma(Args a) {
   using K = RowTma<S, SW, L>;
@@ -149,7 +182,12 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
     }
     mbar_wait(&bars[s], parity);
     double2 v[1][E];
-    if constexpr (SW == 1) {
+    constexpr bool SPLIT = (SW == 1 && S == EM_SUB && CH == 2 && K::ST_ROWS == 0);
+    if constexpr (SPLIT) {
+      // ---- prologue, each element once (see em_sub_prologue_half) ----
+      if (ch == 0) em_sub_prologue_half<0, L, E, NQ>(a, v, st, chi_s, xbuf, t, c, off, dl, acc);
+      else em_sub_prologue_half<1, L, E, NQ>(a, v, st, chi_s, st, t, c, off, dl, acc);
+    } else if constexpr (SW == 1) {
       // ---- prologue: fields to transform (solvers.py:303-311 / :398-420) ----
 #pragma unroll
       for (int i = 0; i < E; ++i) {
@@ -196,6 +234,17 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
     }
     __syncthreads();  // the main row becomes exchange scratch
     double2* xb = (CH == 2 && ch == 1) ? (K::ST_ROWS ? st + K::ST_OFF : xbuf) : st;
+    if constexpr (SPLIT) {
+      // the partner's half of this channel, staged in this channel's buffer
+      if (ch == 0) {
+#pragma unroll
+        for (int k = 0; k < E / 2; ++k) v[0][E / 2 + k] = st[pos_first<L, E>(false, t, E / 2 + k)];
+      } else {
+#pragma unroll
+        for (int k = 0; k < E / 2; ++k) v[0][k] = xbuf[pos_first<L, E>(false, t, k)];
+      }
+      HalfSync{1 + ch, T}();  // every staged value is read before the first exchange overwrites it
+    }
     if constexpr (CH == 2) {
       // the two channels transform in separate buffers: each synchronises
       // only its own T threads (named barrier 1 + ch), not the whole CTA
