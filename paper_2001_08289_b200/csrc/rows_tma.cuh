@@ -258,48 +258,71 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
       for (int i = 0; i < E; ++i) OUT[woff + pos_last<L, E>(false, t, i)] = v[0][i];
     } else {
       // ---- epilogue: state update for iteration k+1 (solvers.py:303-308, :398-411) ----
+      // Elements go in batches of NB: the batch's phase-1 state loads (L2-
+      // prefetched) are all issued before its stores, so a thread waits for
+      // the load latency E/NB times per line instead of once per element
+      // (the stores may alias the loads, so the compiler cannot hoist them).
+      constexpr int NB = 4;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int x = pos_last<L, E>(true, t, i);
-        const bool in1 = chi_s[x] != 0;
-        const double2 gq = cscale(v[0][i], a.inv_n);
-        double2 qn;
-        if constexpr (S == BASIC) {
-          qn = csub(cadd(st[K::LP + x], dl), cmul(gq, a.inv_s0));
-          a.X[0][off + x] = qn;
-        } else if constexpr (S == EM) {
-          qn = cmul(cadd(a.two_s0_e0[c], gq), in1 ? a.inv_sum1 : a.inv_sum2);
-          a.X[0][off + x] = qn;
-        } else if constexpr (S == BASIC_SUB) {
-          const double2 q = st[K::LP + x];
-          qn = csub(cadd(q, dl), cmul(gq, a.inv_s0));
-          a.X[0][off + x] = qn;
-          if (in1) {
-            const double2 sv = a.X[1][off + x];
-            const AugFlux f = apply_A(a, true, q, sv, czero());
-            double2 jq, js;
-            pinned_flux(a, true, f.jq, f.js, dl, jq, js);
-            a.X[1][off + x] = csub(sv, cmul(js, a.inv_s0));
-          }
-        } else {
-          const double2 wq = cadd(a.two_s0_e0[c], gq);
-          double2 ws = czero(), wt = czero();
-          if (in1) {
-            const double2 q = a.X[0][off + x], sv = a.X[1][off + x], tv = a.X[2][off + x];
-            const AugFlux f = apply_A(a, true, q, sv, tv);
-            const double2 rs = csub(f.js, cmul(a.s0, sv));
-            ws = make_double2(-rs.x, -rs.y);
-            wt = csub(f.jt, cmul(a.s0, tv));
-          }
-          double2 sn, tn;
-          em_sub_update(a, in1, wq, ws, wt, qn, sn, tn);
-          a.X[0][off + x] = qn;
-          if (in1) {
-            a.X[1][off + x] = sn;
-            a.X[2][off + x] = tn;
+      for (int b0 = 0; b0 < E; b0 += NB) {
+        double2 qv[NB], sv[NB], tv[NB];
+        bool in1v[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int x = pos_last<L, E>(true, t, b0 + u);
+          in1v[u] = chi_s[x] != 0;
+          qv[u] = sv[u] = tv[u] = czero();
+          if constexpr (S == BASIC_SUB) {
+            if (in1v[u]) sv[u] = a.X[1][off + x];
+          } else if constexpr (S == EM_SUB) {
+            if (in1v[u]) {
+              qv[u] = a.X[0][off + x];
+              sv[u] = a.X[1][off + x];
+              tv[u] = a.X[2][off + x];
+            }
           }
         }
-        acc_c<NQ>(acc, c, qn);
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int x = pos_last<L, E>(true, t, b0 + u);
+          const bool in1 = in1v[u];
+          const double2 gq = cscale(v[0][b0 + u], a.inv_n);
+          double2 qn;
+          if constexpr (S == BASIC) {
+            qn = csub(cadd(st[K::LP + x], dl), cmul(gq, a.inv_s0));
+            a.X[0][off + x] = qn;
+          } else if constexpr (S == EM) {
+            qn = cmul(cadd(a.two_s0_e0[c], gq), in1 ? a.inv_sum1 : a.inv_sum2);
+            a.X[0][off + x] = qn;
+          } else if constexpr (S == BASIC_SUB) {
+            const double2 q = st[K::LP + x];
+            qn = csub(cadd(q, dl), cmul(gq, a.inv_s0));
+            a.X[0][off + x] = qn;
+            if (in1) {
+              const AugFlux f = apply_A(a, true, q, sv[u], czero());
+              double2 jq, js;
+              pinned_flux(a, true, f.jq, f.js, dl, jq, js);
+              a.X[1][off + x] = csub(sv[u], cmul(js, a.inv_s0));
+            }
+          } else {
+            const double2 wq = cadd(a.two_s0_e0[c], gq);
+            double2 ws = czero(), wt = czero();
+            if (in1) {
+              const AugFlux f = apply_A(a, true, qv[u], sv[u], tv[u]);
+              const double2 rs = csub(f.js, cmul(a.s0, sv[u]));
+              ws = make_double2(-rs.x, -rs.y);
+              wt = csub(f.jt, cmul(a.s0, tv[u]));
+            }
+            double2 sn, tn;
+            em_sub_update(a, in1, wq, ws, wt, qn, sn, tn);
+            a.X[0][off + x] = qn;
+            if (in1) {
+              a.X[1][off + x] = sn;
+              a.X[2][off + x] = tn;
+            }
+          }
+          acc_c<NQ>(acc, c, qn);
+        }
       }
     }
     __syncthreads();  // stage s fully consumed (exchange, chi, X0 row)
