@@ -107,25 +107,36 @@ template <int H, int L, int E, int NQ>
 __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)[1][E], const double2* st,
                                                      const uint8_t* chi_s, double2* other, int t, int c, size_t off,
                                                      double2 dl, double (&acc)[NQ]) {
+  // S/T loads (phase 1 only, L2-prefetched) in batches of NB issued ahead of
+  // the batch's staging stores; interleaved with them each would wait one latency
+  constexpr int NB = 4;
 #pragma unroll
-  for (int k = 0; k < E / 2; ++k) {
-    const int i = H * (E / 2) + k;
-    const int x = pos_first<L, E>(false, t, i);
-    const bool in1 = chi_s[x] != 0;
-    const double2 q = st[x];
-    double2 sv = czero(), tv = czero();
-    if (in1) {
-      sv = a.X[1][off + x];
-      tv = a.X[2][off + x];
+  for (int k0 = 0; k0 < E / 2; k0 += NB) {
+    double2 sv[NB], tv[NB];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int x = pos_first<L, E>(false, t, H * (E / 2) + k0 + u);
+      sv[u] = tv[u] = czero();
+      if (chi_s[x] != 0) {
+        sv[u] = a.X[1][off + x];
+        tv[u] = a.X[2][off + x];
+      }
     }
-    const AugFlux f = apply_A(a, in1, q, sv, tv);
-    double2 jq, js;
-    pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
-    acc_c<NQ>(acc, c, jq);
-    if (in1) acc[NQ - 1] += cabs2(js);
-    const double2 rq = csub(f.jq, cmul(a.s0, q));
-    v[0][i] = H == 0 ? rq : jq;
-    other[x] = H == 0 ? jq : rq;
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int i = H * (E / 2) + k0 + u;
+      const int x = pos_first<L, E>(false, t, i);
+      const bool in1 = chi_s[x] != 0;
+      const double2 q = st[x];
+      const AugFlux f = apply_A(a, in1, q, sv[u], tv[u]);
+      double2 jq, js;
+      pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
+      acc_c<NQ>(acc, c, jq);
+      if (in1) acc[NQ - 1] += cabs2(js);
+      const double2 rq = csub(f.jq, cmul(a.s0, q));
+      v[0][i] = H == 0 ? rq : jq;
+      other[x] = H == 0 ? jq : rq;
+    }
   }
 }
 
