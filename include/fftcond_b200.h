@@ -208,8 +208,15 @@ typedef struct fftc_kstat {
 void fftc_profile(int32_t enable);
 int fftc_kernel_stats(fftc_kstat* out, int32_t max_entries);
 
-/* 1 if an axis of length n is supported by the compiled transforms. */
+/* 1 if fftc_solve accepts an axis of length n: even and >= 2, the
+ * reference's PhaseMap rule (geometry.py:37). */
 int fftc_supported_length(int64_t n);
+
+/* 1 if an axis of length n runs the fused sweeps (powers of two 2..4096).
+ * fftc_solve runs grids with any other even axis on the general path
+ * (pointwise kernels around cuFFT); the operator entry points (fftc_fft,
+ * fftc_gamma1, ...) need fused lengths. */
+int fftc_fused_length(int64_t n);
 
 /* Description of the last error on this thread ("" if none). */
 const char* fftc_last_error(void);

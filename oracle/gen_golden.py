@@ -8,7 +8,7 @@ come from the reference (it is 2-D only, geometry.py:33-34); they come from
 ``oracle/fftcond_oracle.py`` and say so in their ``source`` field.
 
 Usage:  python oracle/gen_golden.py <group> [<group> ...] [--jobs N]
-Groups: edge, c1, c2small, c5small, c2full, c5full, 3d, fields
+Groups: edge, c1, c2small, c5small, c2full, c5full, 3d, fields, general
 """
 
 from __future__ import annotations
@@ -233,6 +233,27 @@ def groups():
     for c in three:
         c["force_oracle"] = True
     g["3d"] = three
+
+    # grids outside the fused transforms' power-of-two lengths (the general
+    # path: pointwise kernels around cuFFT); 2-D from the live reference
+    gen = []
+    for sch in ("basic", "em", "basic_sub", "em_sub"):
+        gen.append(C(f"gen_sq6_{sch}", dict(kind="square", n=6, side=2), sch, 10.0, tol=1e-10, max_iters=2000))
+        gen.append(C(f"gen_sq48_{sch}", sq(48), sch, 10.0, tol=1e-10, max_iters=5000))
+        gen.append(C(f"gen_sq96_{sch}_s1000", sq(96), sch, 1000.0, tol=1e-8, max_iters=20000))
+        gen.append(C(f"gen_rect40x24_{sch}", dict(kind="rect", ny=40, nx=24, my=10, mx=8), sch, 3.0 + 1.0j,
+                     tol=1e-10, max_iters=5000))
+        gen.append(C(f"gen_random30x50_{sch}", dict(kind="random", ny=30, nx=50, frac=0.3, seed=SEED), sch,
+                     20.0 + 5.0j, tol=1e-10, max_iters=5000))
+    three_gen = []
+    for sch in ("basic", "em", "basic_sub", "em_sub"):
+        three_gen.append(C(f"gen3d_random12_{sch}", dict(kind="random3d", n=12, frac=0.3, seed=SEED), sch, 50.0,
+                           tol=1e-8, max_iters=5000, e0=[[1 / math.sqrt(3), 0]] * 3))
+        three_gen.append(C(f"gen3d_cube24_{sch}", dict(kind="cube", n=24, side=14), sch, 100.0, tol=1e-8,
+                           max_iters=5000, e0=[[1, 0], [0, 0], [0, 0]]))
+    for c in three_gen:
+        c["force_oracle"] = True
+    g["general"] = gen + three_gen
     return g
 
 

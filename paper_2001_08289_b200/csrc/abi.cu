@@ -23,6 +23,9 @@
 #include "host_common.h"
 #include "kernel_table.h"
 #include "sweeps.cuh"
+#include "general.cuh"
+
+#include <cufft.h>
 
 using namespace fftc;
 
@@ -58,6 +61,15 @@ int lg2_exact(long long n) {
   int lg = 0;
   while ((1LL << lg) < n) ++lg;
   return lg <= MAX_LG ? lg : -1;
+}
+
+// an axis the solve accepts: even and >= 2, as the reference's PhaseMap
+bool even_axis(long long n) { return n >= 2 && n % 2 == 0 && n <= (1LL << 30); }
+// grids the fused sweeps do not cover go through general.cuh + cuFFT
+bool general_grid(int d, long long nx, long long ny, long long nz) {
+  if (const char* e = getenv("FFTC_GENERAL"))
+    if (atoi(e) == 1) return true;
+  return lg2_exact(nx) < 0 || lg2_exact(ny) < 0 || (d == 3 && lg2_exact(nz) < 0);
 }
 
 // exp(-2 pi i m / L), m = 0..L-1, in long double then rounded
@@ -513,7 +525,8 @@ const char* fftc_last_error(void) { return g_err.c_str(); }
 int fftc_version(void) { return 100; }
 int64_t fftc_launch_count(void) { return g_launches.load(); }
 int32_t fftc_last_layout(void) { return g_last_zbs; }
-int fftc_supported_length(int64_t n) { return lg2_exact(n) > 0 ? 1 : 0; }
+int fftc_supported_length(int64_t n) { return even_axis(n) ? 1 : 0; }
+int fftc_fused_length(int64_t n) { return lg2_exact(n) > 0 ? 1 : 0; }
 
 void fftc_profile(int32_t enable) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -547,11 +560,15 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     return 2;
   }
   const long long nx = pb->n[0], ny = pb->n[1], nz = d == 3 ? pb->n[2] : 1;
-  const int lgx = lg2_exact(nx), lgy = lg2_exact(ny), lgz = d == 3 ? lg2_exact(nz) : 0;
-  if (lgx < 0 || lgy < 0 || lgz < 0) {
-    g_err = "unsupported grid: every axis must be a power of two in [2, 4096]";
+  if (!even_axis(nx) || !even_axis(ny) || (d == 3 && !even_axis(nz))) {
+    g_err = "unsupported grid: every axis must be even and >= 2 (reference geometry.py:37)";
     return 3;
   }
+  // powers of two 2..4096 run the fused sweeps; other even lengths (or
+  // FFTC_GENERAL=1) the general path of general.cuh around cuFFT
+  const bool general = general_grid(d, nx, ny, nz);
+  const int lgx = general ? 1 : lg2_exact(nx), lgy = general ? 1 : lg2_exact(ny),
+            lgz = general ? (d == 3 ? 1 : 0) : (d == 3 ? lg2_exact(nz) : 0);
   if (pr->scheme < 0 || pr->scheme > 3) {
     g_err = "bad scheme";
     return 2;
@@ -581,7 +598,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     // (FFTC_DEBUG_SYNC synchronises after every launch: not allowed in a capture)
-    use_graph = !g_profile && pr->max_iters <= (1 << 20) && !getenv("FFTC_NO_GRAPH") && !debug_sync();
+    use_graph = !general && !g_profile && pr->max_iters <= (1 << 20) && !getenv("FFTC_NO_GRAPH") && !debug_sync();
   }
   // graph mode runs the whole loop in one launch: the device keeps every record
   const int hist_ring = use_graph ? (int)std::max<int64_t>(pr->max_iters, 16) : 1024;
@@ -626,8 +643,27 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   const LTable& TZ = R.tab[d == 3 ? lgz : lgy];
   long long nrec_host = 0;
   bool stopped = false;
+  cufftHandle plan = 0;  // general path: batched d-component transform (cuFFT)
 
   do {
+    if (general) {
+      long long n[3];
+      if (d == 2) {
+        n[0] = ny;
+        n[1] = nx;
+      } else {
+        n[0] = nz;
+        n[1] = ny;
+        n[2] = nx;
+      }
+      size_t wsz = 0;
+      if (cufftCreate(&plan) != CUFFT_SUCCESS ||
+          cufftMakePlanMany64(plan, d, n, nullptr, 1, N, nullptr, 1, N, CUFFT_Z2Z, d, &wsz) != CUFFT_SUCCESS) {
+        g_err = "cuFFT plan for the general grid failed";
+        rc = 1;
+        break;
+      }
+    }
     CK(cudaMemsetAsync(a.st, 0, sizeof(DevState), s));
     CK(cudaEventRecord(ev0, s));
     {
@@ -685,7 +721,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     const PeerOut* no_peer = nullptr;
     a.zbs = 0;
     g_last_zbs = 0;
-    if (d == 3) {
+    if (d == 3 && !general) {
       // z-blocked work fields when all three column passes run on TMA tiles
       const int zbs = zblock_shift(nx, ny, nz);
       const KInfo& kz = TZ.col[em_type ? KC_MID3T_EM : KC_MID3T_BASIC];
@@ -711,8 +747,42 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     void** amid = use_tma_mid ? amid_tma : amid_std;
     ColGeom yfB = yf;  // forward y pass of field B (em-type) uses the same geometry
 
+    // general grids: prologue, cuFFT forward, Gamma^ + monitor, cuFFT
+    // inverse, epilogue (general.cuh)
+    auto launch_gen = [&](Launcher& L) -> int {
+      int r = 0;
+      switch (scheme) {
+        case FFTC_BASIC: r = launch_elementwise(k_gen_pro<BASIC>, L, (long long)d * N, a, K_SWEEP1); break;
+        case FFTC_EM: r = launch_elementwise(k_gen_pro<EM>, L, (long long)d * N, a, K_SWEEP1); break;
+        case FFTC_BASIC_SUB: r = launch_elementwise(k_gen_pro<BASIC_SUB>, L, (long long)d * N, a, K_SWEEP1); break;
+        default: r = launch_elementwise(k_gen_pro<EM_SUB>, L, (long long)d * N, a, K_SWEEP1); break;
+      }
+      if (r) return r;
+      if (cufftSetStream(plan, L.s) != CUFFT_SUCCESS ||
+          cufftExecZ2Z(plan, (cufftDoubleComplex*)a.A, (cufftDoubleComplex*)a.A, CUFFT_FORWARD) != CUFFT_SUCCESS ||
+          (em_type &&
+           cufftExecZ2Z(plan, (cufftDoubleComplex*)a.B, (cufftDoubleComplex*)a.B, CUFFT_FORWARD) != CUFFT_SUCCESS)) {
+        g_err = "cuFFT forward transform failed";
+        return 1;
+      }
+      r = em_type ? launch_elementwise(k_gen_gamma<MID_EM>, L, N, a, K_MID)
+                  : launch_elementwise(k_gen_gamma<MID_BASIC>, L, N, a, K_MID);
+      if (r) return r;
+      if (cufftExecZ2Z(plan, (cufftDoubleComplex*)a.A, (cufftDoubleComplex*)a.A, CUFFT_INVERSE) != CUFFT_SUCCESS) {
+        g_err = "cuFFT inverse transform failed";
+        return 1;
+      }
+      switch (scheme) {
+        case FFTC_BASIC: return launch_elementwise(k_gen_epi<BASIC>, L, (long long)d * N, a, K_SWEEP3);
+        case FFTC_EM: return launch_elementwise(k_gen_epi<EM>, L, (long long)d * N, a, K_SWEEP3);
+        case FFTC_BASIC_SUB: return launch_elementwise(k_gen_epi<BASIC_SUB>, L, (long long)d * N, a, K_SWEEP3);
+        default: return launch_elementwise(k_gen_epi<EM_SUB>, L, (long long)d * N, a, K_SWEEP3);
+      }
+    };
+
     // one reference iteration (solvers.py:300-321 / :395-432) = these launches
     auto launch_iter = [&](Launcher& L) -> int {
+      if (general) return launch_gen(L);
       int r = L.go(TX.s1[scheme], row_lines, a1, K_SWEEP1);
       if (r) return r;
       if (d == 3) {
@@ -878,6 +948,10 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       out->mean_J[c][1] = c < d ? hst->meanJ[c].y : 0.0;
     }
   } while (0);
+  if (plan) {
+    cudaStreamSynchronize(s);  // the plan's work area may still be in use
+    cufftDestroy(plan);
+  }
   out->kernel_launches = Lc.count;
   g_launches += Lc.count;
   cudaFreeAsync(ws, s);

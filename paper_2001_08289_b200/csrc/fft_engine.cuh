@@ -317,7 +317,7 @@ __device__ __forceinline__ void stage_compute(double2 (&v)[C][E], const StageTw<
 // Exchange between stage S and S+1 through shared memory.  `buf(c)` is the
 // padded buffer of channel c for this transform.  `bar` synchronises all
 // threads sharing the buffers (normally __syncthreads).
-template <int L, int E, int C, bool INV, int S, class Buf, class Bar>
+template <int L, int E, int C, bool INV, int S, class Buf, class Bar, bool TAIL = true>
 __device__ __forceinline__ void stage_exchange(double2 (&v)[C][E], int t, Buf buf, Bar bar) {
   using P = Plan<L, E>;
   constexpr int R = P::radix(INV, S);
@@ -369,10 +369,10 @@ __device__ __forceinline__ void stage_exchange(double2 (&v)[C][E], int t, Buf bu
         for (int c = 0; c < C; ++c) v[c][b * R2 + r] = buf(c)[padpos<P::PS>(j + r * LD_STRIDE)];
     }
   }
-  bar();
+  if constexpr (TAIL) bar();
 }
 
-template <int L, int E, int C, bool INV, int S, class Buf, class Bar, class TW>
+template <int L, int E, int C, bool INV, int S, bool TAIL, class Buf, class Bar, class TW>
 __device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, TW tw, Buf buf, Bar bar,
                                          const StageTw<L, E, INV, S>& tws) {
   using P = Plan<L, E>;
@@ -380,17 +380,19 @@ __device__ __forceinline__ void run_from(double2 (&v)[C][E], int t, TW tw, Buf b
   if constexpr (S + 1 < P::NST) {
     StageTw<L, E, INV, S + 1> nxt;
     nxt.load(t, tw);  // in flight during the exchange
-    stage_exchange<L, E, C, INV, S>(v, t, buf, bar);
-    run_from<L, E, C, INV, S + 1>(v, t, tw, buf, bar, nxt);
+    stage_exchange<L, E, C, INV, S, Buf, Bar, (TAIL || S + 2 < P::NST)>(v, t, buf, bar);
+    run_from<L, E, C, INV, S + 1, TAIL>(v, t, tw, buf, bar, nxt);
   }
 }
 
 // Full length-L transform of C channels.  Input: element i of thread t sits
 // at pos_first(INV,t,i); output: element i at pos_last(INV,t,i).
-template <int L, int E, int C, bool INV, class Buf, class Bar, class TW>
+// TAIL = false drops the barrier after the last exchange's reads: only for
+// callers that pass another barrier before anything writes the buffer again.
+template <int L, int E, int C, bool INV, bool TAIL = true, class Buf, class Bar, class TW>
 __device__ __forceinline__ void fft_line(double2 (&v)[C][E], int t, TW tw, Buf buf, Bar bar) {
   StageTw<L, E, INV, 0> first;  // stage 0 has Ns = 1: no twiddles
-  run_from<L, E, C, INV, 0>(v, t, tw, buf, bar, first);
+  run_from<L, E, C, INV, 0, TAIL>(v, t, tw, buf, bar, first);
 }
 
 // ----------------------------------------------------------------------------

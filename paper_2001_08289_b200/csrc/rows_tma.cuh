@@ -259,9 +259,11 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
     if constexpr (CH == 2) {
       // the two channels transform in separate buffers: each synchronises
       // only its own T threads (named barrier 1 + ch), not the whole CTA
-      fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, HalfSync{1 + ch, T});
+      // (no barrier after the last exchange: the __syncthreads closing the
+      // line comes before the buffer is written again)
+      fft_line<L, E, 1, INV, false>(v, t, a.tw[0], SmemBuf{xb, 0}, HalfSync{1 + ch, T});
     } else {
-      fft_line<L, E, 1, INV>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
+      fft_line<L, E, 1, INV, false>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
     }
     if constexpr (SW == 1) {
       const size_t woff = work_off(a, c, row);  // work field row (z-blocked in 3-D)

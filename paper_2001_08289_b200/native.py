@@ -22,6 +22,7 @@ EXPORTS = (
     "fftc_solve",
     "fftc_solve_host",
     "fftc_supported_length",
+    "fftc_fused_length",
     "fftc_last_error",
     "fftc_version",
     "fftc_launch_count",
@@ -148,6 +149,8 @@ def lib():
         L.fftc_kernel_stats.restype = C.c_int
         L.fftc_supported_length.argtypes = [i64]
         L.fftc_supported_length.restype = C.c_int
+        L.fftc_fused_length.argtypes = [i64]
+        L.fftc_fused_length.restype = C.c_int
         L.fftc_last_error.argtypes = []
         L.fftc_last_error.restype = C.c_char_p
         L.fftc_version.restype = C.c_int

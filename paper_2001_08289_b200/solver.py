@@ -216,9 +216,7 @@ def _check_grid(pmap: PhaseMap):
     L = native.lib()
     for n in pmap.grid:
         if not L.fftc_supported_length(int(n)):
-            raise ContractError(
-                f"grid axis of length {n} is not supported by the B200 transforms "
-                "(power-of-two lengths 2..4096)")
+            raise ContractError(f"grid axis of length {n} is not supported (even lengths >= 2)")
 
 
 def _problem(pmap: PhaseMap, chi) -> native.Problem:

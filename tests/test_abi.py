@@ -34,9 +34,11 @@ def test_version_and_lengths():
     L = native.lib()
     assert L.fftc_version() >= 100
     for n in (2, 4, 64, 256, 1024, 2048, 4096):
-        assert L.fftc_supported_length(n) == 1
-    for n in (0, 1, 3, 6, 12, 8192, 100):
-        assert L.fftc_supported_length(n) == 0
+        assert L.fftc_supported_length(n) == 1 and L.fftc_fused_length(n) == 1
+    for n in (6, 12, 100, 8192, 3000):  # even: the general path (cuFFT)
+        assert L.fftc_supported_length(n) == 1 and L.fftc_fused_length(n) == 0
+    for n in (0, 1, 3, 7, 101):
+        assert L.fftc_supported_length(n) == 0 and L.fftc_fused_length(n) == 0
     assert L.fftc_last_error() is not None
 
 
@@ -62,6 +64,6 @@ def test_bad_arguments_are_errors_not_crashes():
     assert rc != 0
     assert b"d must be 2 or 3" in L.fftc_last_error()
     p.d = 2
-    p.n[0], p.n[1], p.n[2] = 6, 8, 1  # non power of two
+    p.n[0], p.n[1], p.n[2] = 7, 8, 1  # odd axis: the reference's PhaseMap rejects it too
     rc = L.fftc_solve(C.byref(p), C.byref(par), None, 0, None, None, None, C.byref(res), None)
     assert rc == 3

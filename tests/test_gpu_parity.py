@@ -196,3 +196,23 @@ def test_3d_zblocked_work_layout_bit_identical(shape, scheme, monkeypatch):
         runs[zb] = [(h.sigma_star, h.residual) for h in r.history]
     for zb in ("5", "3", "8"):
         assert runs[zb] == runs["0"], zb
+
+
+@pytest.mark.parametrize("g", _cases("general"))
+def test_general_grids(g):
+    """Even axis lengths outside the fused transforms (6, 24, 30, 40, 48, 50,
+    96, 12^3, 24^3): the general path (general.cuh around cuFFT) against the
+    live reference (2-D) and the oracle (3-D)."""
+    from paper_2001_08289_b200 import native
+
+    assert not all(native.lib().fftc_fused_length(n) for n in _chi(g["case"]["geom"]).shape)
+    check(run_case(g["case"]), g)
+
+
+@pytest.mark.parametrize("g", _cases("c2small", lambda v: v["case"]["geom"]["n"] == 64) + _cases("c1")
+                         + _cases("3d", lambda v: "16" in v["case"]["name"]))
+def test_general_path_on_fused_grids(g, monkeypatch):
+    """FFTC_GENERAL=1 runs power-of-two grids on the general path: same
+    goldens, same iteration counts as the fused sweeps."""
+    monkeypatch.setenv("FFTC_GENERAL", "1")
+    check(run_case(g["case"]), g)

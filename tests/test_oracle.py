@@ -38,7 +38,8 @@ def _params(group, pred=lambda g: True):
     return [pytest.param(v, id=k) for k, v in load_group(group).items() if pred(v)]
 
 
-@pytest.mark.parametrize("g", _params("edge", _small) + _params("c1"))
+@pytest.mark.parametrize("g", _params("edge", _small) + _params("c1")
+                         + _params("general", lambda g: g["source"].startswith("reference") and _small(g)))
 def test_oracle_bit_identical_to_reference(g):
     """d = 2: the restatement reproduces the live reference bit for bit."""
     if g["source"].startswith("oracle"):
