@@ -213,9 +213,8 @@ int fftc_kernel_stats(fftc_kstat* out, int32_t max_entries);
 int fftc_supported_length(int64_t n);
 
 /* 1 if an axis of length n runs the fused sweeps (powers of two 2..4096).
- * fftc_solve runs grids with any other even axis on the general path
- * (pointwise kernels around cuFFT); the operator entry points (fftc_fft,
- * fftc_gamma1, ...) need fused lengths. */
+ * Grids with any other even axis run the general path (pointwise kernels
+ * around cuFFT) in fftc_solve, fftc_fft and fftc_gamma1. */
 int fftc_fused_length(int64_t n);
 
 /* Description of the last error on this thread ("" if none). */

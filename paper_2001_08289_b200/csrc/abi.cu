@@ -974,6 +974,7 @@ namespace {
 struct GridInfo {
   int d, lgx, lgy, lgz;
   long long nx, ny, nz, N;
+  bool general;  // an axis outside the fused lengths: cuFFT + general.cuh
 };
 int grid_info(const fftc_problem* pb, GridInfo& g) {
   if (!pb || (pb->d != 2 && pb->d != 3)) {
@@ -984,14 +985,69 @@ int grid_info(const fftc_problem* pb, GridInfo& g) {
   g.nx = pb->n[0];
   g.ny = pb->n[1];
   g.nz = g.d == 3 ? pb->n[2] : 1;
-  g.lgx = lg2_exact(g.nx);
-  g.lgy = lg2_exact(g.ny);
-  g.lgz = g.d == 3 ? lg2_exact(g.nz) : 0;
-  if (g.lgx < 0 || g.lgy < 0 || g.lgz < 0) {
-    g_err = "unsupported grid: every axis must be a power of two in [2, 4096]";
+  if (!even_axis(g.nx) || !even_axis(g.ny) || (g.d == 3 && !even_axis(g.nz))) {
+    g_err = "unsupported grid: every axis must be even and >= 2 (reference geometry.py:37)";
     return 3;
   }
+  g.general = general_grid(g.d, g.nx, g.ny, g.nz);
+  g.lgx = g.general ? 1 : lg2_exact(g.nx);
+  g.lgy = g.general ? 1 : lg2_exact(g.ny);
+  g.lgz = g.d == 3 ? (g.general ? 1 : lg2_exact(g.nz)) : 0;
   g.N = g.nx * g.ny * g.nz;
+  return 0;
+}
+
+// general grids: unnormalised cuFFT transforms of a (d, grid) field in place,
+// all axes (mask 2^d - 1: one batched rank-d plan) or axis by axis
+int cufft_axes(double2* data, const GridInfo& g, int mask, bool inverse, cudaStream_t s) {
+  const int dir = inverse ? CUFFT_INVERSE : CUFFT_FORWARD;
+  auto run = [&](int rank, long long* n, long long istride, long long idist, long long batch, long long nblocks,
+                 long long bstride) -> int {
+    cufftHandle plan = 0;
+    size_t wsz = 0;
+    int rc = 0;
+    if (cufftCreate(&plan) != CUFFT_SUCCESS ||
+        cufftMakePlanMany64(plan, rank, n, n, istride, idist, n, istride, idist, CUFFT_Z2Z, batch, &wsz) !=
+            CUFFT_SUCCESS ||
+        cufftSetStream(plan, s) != CUFFT_SUCCESS) {
+      g_err = "cuFFT plan failed";
+      rc = 1;
+    }
+    for (long long b = 0; !rc && b < nblocks; ++b) {
+      cufftDoubleComplex* p = (cufftDoubleComplex*)(data + b * bstride);
+      if (cufftExecZ2Z(plan, p, p, dir) != CUFFT_SUCCESS) {
+        g_err = "cuFFT transform failed";
+        rc = 1;
+      }
+    }
+    if (plan) {
+      cudaStreamSynchronize(s);  // the plan's work area may still be in use
+      cufftDestroy(plan);
+    }
+    return rc;
+  };
+  const int all = (1 << g.d) - 1;
+  if ((mask & all) == all) {
+    long long n[3];
+    if (g.d == 2) {
+      n[0] = g.ny;
+      n[1] = g.nx;
+    } else {
+      n[0] = g.nz;
+      n[1] = g.ny;
+      n[2] = g.nx;
+    }
+    return run(g.d, n, 1, g.N, g.d, 1, 0);
+  }
+  for (int ax = 0; ax < g.d; ++ax) {
+    if (!(mask & (1 << ax))) continue;
+    long long n[1] = {ax == 0 ? g.nx : (ax == 1 ? g.ny : g.nz)};
+    const long long stride = ax == 0 ? 1 : (ax == 1 ? g.nx : g.nx * g.ny);
+    const long long block = n[0] * stride;  // contiguous elements holding `stride` interleaved lines
+    const long long nblocks = (long long)g.d * g.N / block;
+    int rc = stride == 1 ? run(1, n, 1, n[0], nblocks, 1, 0) : run(1, n, stride, 1, stride, nblocks, block);
+    if (rc) return rc;
+  }
   return 0;
 }
 
@@ -1064,6 +1120,11 @@ int fftc_fft(const fftc_problem* pb, void* data, int32_t inverse, int32_t axes_m
   a.tw[1] = R.tw[g.lgy];
   a.tw[2] = g.d == 3 ? R.tw[g.lgz] : R.tw[g.lgy];
   cudaStream_t s = (cudaStream_t)stream;
+  if (g.general) {
+    if (int rc = cufft_axes((double2*)data, g, axes_mask, inverse != 0, s)) return rc;
+    CK(cudaGetLastError());
+    return 0;
+  }
   Scratch sc;
   if (sc.alloc(a, R.num_sms, s)) return 1;
   Launcher Lc(s, R.num_sms);
@@ -1101,6 +1162,16 @@ int fftc_gamma1(const fftc_problem* pb, const void* in, void* out, double scale,
   Scratch sc;
   if (sc.alloc(a, R.num_sms, s)) return 1;
   Launcher Lc(s, R.num_sms);
+  if (g.general) {  // cuFFT forward, Gamma^ (scaled by 1/N in operator mode), cuFFT inverse
+    const int all = (1 << g.d) - 1;
+    int rc = cufft_axes(a.A, g, all, false, s);
+    if (!rc) rc = launch_elementwise(k_gen_gamma<MID_BASIC>, Lc, g.N, a, K_OP);
+    if (!rc) rc = cufft_axes(a.A, g, all, true, s);
+    g_launches += Lc.count;
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    return 0;
+  }
   int rc = run_axis(Lc, a, g, 0, false, 1.0);
   if (!rc && g.d == 3) rc = run_axis(Lc, a, g, 1, false, 1.0);
   if (!rc) {
@@ -1140,6 +1211,10 @@ int fftc_debug_project(const fftc_problem* pb, void* data, void* stream) {
   g_err.clear();
   GridInfo g;
   if (int rc = grid_info(pb, g)) return rc;
+  if (g.general) {
+    g_err = "fftc_debug_project: fused (power-of-two) lengths only";
+    return 3;
+  }
   if (ensure_registry()) return 1;
   Registry& R = reg();
   cudaStream_t s = (cudaStream_t)stream;

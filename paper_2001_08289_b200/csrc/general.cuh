@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256) k_gen_gamma(Args a) {
         if constexpr (MODE == MID_BASIC) {
           const double2 g = cscale(dot, k[c]);
           acc[0] += cabs2(cscale(g, a.inv_n));  // Parseval on the 1/N-scaled mode
-          a.A[(size_t)c * a.N + p] = g;
+          // operator mode (fftc_gamma1): the inverse transform's 1/N here
+          a.A[(size_t)c * a.N + p] = a.op_mode ? cscale(g, a.inv_n) : g;
         } else {
           a.A[(size_t)c * a.N + p] = csub(F[c], cscale(dot, 2.0 * k[c]));
         }

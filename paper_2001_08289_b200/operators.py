@@ -37,9 +37,8 @@ def _problem(shape) -> native.Problem:
         raise ContractError(f"expected a (d, *grid) field with d = 2 or 3, got {tuple(shape)}")
     L = native.lib()
     for n in grid:
-        if not L.fftc_fused_length(int(n)):
-            raise ContractError(f"grid axis of length {n} is not supported by the operator kernels "
-                                "(power of two 2..4096; solves accept any even length)")
+        if not L.fftc_supported_length(int(n)):
+            raise ContractError(f"grid axis of length {n} is not supported (even lengths >= 2)")
     p = native.Problem()
     p.d = d
     p.n[0] = grid[-1]

@@ -13,6 +13,9 @@ pytestmark = pytest.mark.gpu
 SHAPES_2D = [(2, 2), (4, 8), (8, 8), (16, 32), (32, 16), (64, 64), (256, 128), (2048, 8), (8, 4096)]
 SHAPES_3D = [(2, 16, 16), (4, 16, 16), (16, 16, 16), (16, 16, 2), (16, 2, 16), (8, 16, 32), (32, 16, 8),
              (2, 2, 2), (64, 32, 16)]
+# even lengths outside the fused transforms: the general path (cuFFT)
+SHAPES_2D += [(6, 10), (48, 30), (100, 2), (6, 8192)]
+SHAPES_3D += [(6, 4, 10), (12, 12, 12), (2, 30, 8)]
 
 
 def _rand(shape, seed=0):
@@ -34,6 +37,20 @@ def test_fft_each_axis(shape, inverse):
         ref = np.fft.ifft(f, axis=np_axis) * shape[np_axis] if inverse else np.fft.fft(f, axis=np_axis)
         err = np.abs(got - ref).max() / np.abs(ref).max()
         assert err < 1e-14, (shape, ax, inverse, err)
+
+
+@pytest.mark.parametrize("shape", [(6, 10), (48, 30), (16, 32), (6, 4, 10), (12, 12, 12), (8, 16, 32)])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_fft_all_axes(shape, inverse):
+    from paper_2001_08289_b200.operators import fft_axes
+
+    f = _rand(shape, 2)
+    d = len(shape)
+    got = fft_axes(f, (1 << d) - 1, inverse).cpu().numpy()
+    axes = tuple(range(1, d + 1))
+    ref = np.fft.ifftn(f, axes=axes) * np.prod(shape) if inverse else np.fft.fftn(f, axes=axes)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-14, (shape, inverse, err)
 
 
 @pytest.mark.parametrize("shape", SHAPES_2D + SHAPES_3D)
