@@ -87,6 +87,46 @@ sigma0_im = 0.5
 history_csv = history.csv
 result_json = result.json
 """),
+    # grids outside the fused power-of-two lengths (the general cuFFT path)
+    "compare_n96": ("compare", """[geometry]
+kind = square
+n = 96
+side_fraction = 0.5
+
+[physics]
+sigma1_re = 2.0
+
+[scheme]
+names = basic, em, basic_sub, em_sub
+alpha = 0.25
+beta = 4.0
+tol = 1e-10
+max_iters = 1000
+
+[output]
+history_csv = history.csv
+summary_csv = summary.csv
+"""),
+    "disk_n100": ("solve", """[geometry]
+kind = disk
+n = 100
+radius = 0.3
+
+[physics]
+sigma1_re = 5.0
+sigma1_im = 2.0
+
+[scheme]
+name = em_sub
+alpha = 0.25
+beta = 4.0
+tol = 1e-10
+max_iters = 1000
+
+[output]
+history_csv = history.csv
+result_json = result.json
+"""),
     # a scheme that errors (branch cut) inside compare
     "compare_branch_cut": ("compare", """[geometry]
 kind = square
@@ -109,7 +149,10 @@ summary_csv = summary.csv
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    only = set(sys.argv[1:])
     for name, (cmd, text) in CASES.items():
+        if only and name not in only:
+            continue
         d = os.path.join(OUT, name)
         shutil.rmtree(d, ignore_errors=True)
         os.makedirs(d)
