@@ -8,7 +8,7 @@ come from the reference (it is 2-D only, geometry.py:33-34); they come from
 ``oracle/fftcond_oracle.py`` and say so in their ``source`` field.
 
 Usage:  python oracle/gen_golden.py <group> [<group> ...] [--jobs N]
-Groups: edge, c1, c2small, c5small, c2full, c5full, 3d, fields, general
+Groups: edge, c1, c2small, c5small, c2full, c5full, 3d, fields, general, big
 """
 
 from __future__ import annotations
@@ -254,6 +254,17 @@ def groups():
     for c in three_gen:
         c["force_oracle"] = True
     g["general"] = gen + three_gen
+
+    # the largest fused lengths (4096) and beyond (8192: the general path)
+    big = [C("big_rect4096x64_em_sub", dict(kind="rect", ny=64, nx=4096, my=32, mx=2048), "em_sub", 10.0,
+             tol=1e-8, max_iters=2000),
+           C("big_rect64x4096_basic", dict(kind="rect", ny=4096, nx=64, my=2048, mx=32), "basic", 10.0 + 1.0j,
+             tol=1e-8, max_iters=2000),
+           C("big_sq4096_em_sub_3it", sq(4096), "em_sub", 10.0, tol=1e-300, max_iters=3),
+           C("big_sq4096_em_3it", sq(4096), "em", 1000.0, tol=1e-300, max_iters=3),
+           C("big_rect8x8192_basic_sub", dict(kind="rect", ny=8, nx=8192, my=4, mx=4096), "basic_sub", 10.0,
+             tol=1e-8, max_iters=2000)]
+    g["big"] = big
     return g
 
 

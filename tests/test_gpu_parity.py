@@ -216,3 +216,11 @@ def test_general_path_on_fused_grids(g, monkeypatch):
     goldens, same iteration counts as the fused sweeps."""
     monkeypatch.setenv("FFTC_GENERAL", "1")
     check(run_case(g["case"]), g)
+
+
+@pytest.mark.parametrize("g", _cases("big"))
+def test_largest_lengths(g):
+    """Axes at the fused maximum (4096: 4096 x 64, 64 x 4096, 4096^2 for three
+    iterations) and beyond it (8192: the general path), against the live
+    reference."""
+    check(run_case(g["case"]), g)
