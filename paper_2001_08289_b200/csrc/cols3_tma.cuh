@@ -20,6 +20,7 @@
 // columns of the same rows.
 #pragma once
 #include "cols_tma.cuh"
+#include "kernel_table.h"
 
 namespace fftc {
 
@@ -27,7 +28,7 @@ template <int L>
 struct Col3Tma {
   static constexpr int E = 8;
   static constexpr int T = L / E;
-  static constexpr int W = L <= 256 ? 8 : (L <= 512 ? 4 : 2);  // columns per tile
+  static constexpr int W = col3_tile_w(L);  // columns per tile
   static constexpr int NC = 3;
   static constexpr int THREADS = NC * W * T;
   static constexpr int LP = Plan<L, E>::LP;
@@ -35,7 +36,12 @@ struct Col3Tma {
   // 16-B bank groups, and SLOT stays a multiple of 8 entries (128 B)
   static constexpr int XS = LP + (W == 2 ? 4 : 2);
   static constexpr int SLOT = NC * W * XS;  // >= NC*W*L landing
-  static constexpr int NSLOT = 2;
+#ifndef FFTC_COL3_NSLOT
+#define FFTC_COL3_NSLOT 2
+#endif
+  static constexpr int NSLOT_FIT = (232448 - 512 - (L / 2) * 16) / (SLOT * 16);
+  // tiles in flight + the one being transformed (as many as fit, up to FFTC_COL3_NSLOT)
+  static constexpr int NSLOT = FFTC_COL3_NSLOT < NSLOT_FIT ? FFTC_COL3_NSLOT : NSLOT_FIT;
   static constexpr int SMEM = (NSLOT * SLOT + L / 2) * (int)sizeof(double2);
   static constexpr int BOXR = L < 256 ? L : 256;
   static constexpr unsigned TX = (unsigned)(NC * W * L * sizeof(double2));
@@ -95,31 +101,34 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0 && nmine > 0) {
-    int f, o, x0;
-    coords(0, f, o, x0);
-    col3_issue(f == 0 ? &tmA : &tmB, smem, &bars[0], x0, col3_outer(g, o), K::TX);
-  }
+  if (threadIdx.x == 0)
+    for (int j = 0; j < K::NSLOT - 1 && j < nmine; ++j) {
+      int f, o, x0;
+      coords(j, f, o, x0);
+      col3_issue(f == 0 ? &tmA : &tmB, smem + j * K::SLOT, &bars[j], x0, col3_outer(g, o), K::TX);
+    }
   double2* tws = smem + K::NSLOT * K::SLOT;
   for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[g.axis][i]);
   __syncthreads();
   const SmemTw tw{tws};
   double acc = 0.0;
   for (long long k = 0; k < nmine; ++k) {
-    const int s = (int)(k & 1);
+    const int s = (int)(k % K::NSLOT);
     int f, o, x0;
     coords(k, f, o, x0);
     double2* slot = smem + s * K::SLOT;
-    mbar_wait(&bars[s], (unsigned)((k >> 1) & 1));
+    mbar_wait(&bars[s], (unsigned)((k / K::NSLOT) & 1));
     double2 v[1][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) v[0][i] = slot[(comp * L + pos_first<L, E>(INV_ONLY, t, i)) * W + w];
     __syncthreads();  // every input is in registers: the slot becomes exchange scratch
-    if (threadIdx.x == 0 && k + 1 < nmine) {
-      // tile k+1 into the other slot, whose store (tile k-1) was committed one tile ago
+    if (threadIdx.x == 0 && k + K::NSLOT - 1 < nmine) {
+      // tile k+NSLOT-1 into the slot of tile k-1, whose store was committed one tile ago
+      const long long nk = k + K::NSLOT - 1;
+      const int ns = (int)(nk % K::NSLOT);
       int nf, no, nx0;
-      coords(k + 1, nf, no, nx0);
-      col3_issue(nf == 0 ? &tmA : &tmB, smem + (s ^ 1) * K::SLOT, &bars[s ^ 1], nx0, col3_outer(g, no), K::TX);
+      coords(nk, nf, no, nx0);
+      col3_issue(nf == 0 ? &tmA : &tmB, smem + ns * K::SLOT, &bars[ns], nx0, col3_outer(g, no), K::TX);
     }
     double2* xb = slot + (comp * W + w) * K::XS;
     const bool parseval_only = (MODE == MID_EM) && f == 1;

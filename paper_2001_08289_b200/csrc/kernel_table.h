@@ -20,7 +20,10 @@ enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_
        KC_MID3P_BASIC = 12, KC_MID3P_EM = 13, KC_FWD3P = 14,  // the same, outputs to their owning ranks
        KC_COUNT = 15 };
 // columns per TMA tile of the 3-D column passes (cols3_tma.cuh: Col3Tma<L>::W)
-constexpr int col3_tile_w(long long L) { return L <= 256 ? 8 : (L <= 512 ? 4 : 2); }
+#ifndef FFTC_COL3_W512
+#define FFTC_COL3_W512 4
+#endif
+constexpr int col3_tile_w(long long L) { return L <= 256 ? 8 : (L <= 512 ? FFTC_COL3_W512 : 2); }
 
 struct LTable {
   int L = 0;
