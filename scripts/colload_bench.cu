@@ -76,6 +76,51 @@ __global__ void __launch_bounds__(512, 1) k_tma(const __grid_constant__ CUtensor
   if (acc == 12345.678) sink[0] = acc;
 }
 
+template <int NSLOT>
+__global__ void __launch_bounds__(512, 1) k_tma5(const __grid_constant__ CUtensorMap tm, int nlines, unsigned slot_bytes,
+                                                  double* sink) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ uint64_t bars[NSLOT];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < NSLOT; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su(&bars[s])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nmine = blockIdx.x < nlines ? (nlines - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto issue = [&](int k, int s) {
+    const int x = blockIdx.x + k * gridDim.x;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(&bars[s])), "r"(slot_bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5, %6}], [%7];" ::"r"(su(sm + (size_t)s * slot_bytes)),
+        "l"(&tm), "r"(0), "r"(x), "r"(0), "r"(0), "r"(0), "r"(su(&bars[s]))
+        : "memory");
+  };
+  if (tid == 0)
+    for (int s = 0; s < NSLOT && s < nmine; ++s) issue(s, s);
+  double acc = 0.0;
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k % NSLOT;
+    const unsigned par = (unsigned)((k / NSLOT) & 1);
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+            su(&bars[s])),
+        "r"(par)
+        : "memory");
+    const double* d = reinterpret_cast<const double*>(sm + (size_t)s * slot_bytes);
+    for (unsigned i = tid; i < slot_bytes / 8; i += 8 * blockDim.x) acc += d[i];
+    __syncthreads();
+    if (tid == 0 && k + NSLOT < nmine) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + NSLOT, s);
+    }
+  }
+  if (acc == 12345.678) sink[0] = acc;
+}
+
 // LDG: a CTA of 512 threads reads lines of W columns x L rows x 2 comps
 // straight into registers (16 LDG.128 per thread per pass), lane bits
 // [log2 W) = column so one warp instruction covers 32/W rows x 16W bytes
@@ -176,6 +221,41 @@ int main() {
            v.W, 16 * v.W, 256 * v.rows_per_box_blocks, v.comp_per_box, v.nslot, slot, 1e3 * ms / reps,
            moved / (1e6 * ms / reps), (double)nlines * 256 * v.rows_per_box_blocks * v.comp_per_box /
                                            (1e-3 * ms / reps * 1.9e9 * nsm));
+  }
+  // row-pair interleaved field: element (c, y, x) at c*L*L + ((y>>1)*L + x)*2 + (y&1); a column's box is
+  // {4 doubles = rows 2m, 2m+1} x {1 x} x {128 pairs} x {8 pair blocks} x {comps}: 32-byte rows
+  for (int ns : {1, 2, 3}) {
+    CUtensorMap tm;
+    const int lo = 128, hi = L / 2 / lo;
+    cuuint64_t dims[5] = {4, (cuuint64_t)L, (cuuint64_t)lo, (cuuint64_t)hi, (cuuint64_t)NC};
+    cuuint64_t strides[4] = {32, (cuuint64_t)32 * L, (cuuint64_t)32 * L * lo, (cuuint64_t)16 * L * L};
+    cuuint32_t box[5] = {4, 1, (cuuint32_t)lo, (cuuint32_t)hi, 2};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, f, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("pair map encode failed %d\n", (int)r); break; }
+    const unsigned slot = (unsigned)(2 * L * 16);
+    const size_t smem = (size_t)slot * ns;
+    const int nlines = L;
+    auto launch = [&]() {
+      if (ns == 1) { cudaFuncSetAttribute(k_tma5<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                     k_tma5<1><<<nsm, 512, smem>>>(tm, nlines, slot, sink); }
+      else if (ns == 2) { cudaFuncSetAttribute(k_tma5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                     k_tma5<2><<<nsm, 512, smem>>>(tm, nlines, slot, sink); }
+      else { cudaFuncSetAttribute(k_tma5<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                     k_tma5<3><<<nsm, 512, smem>>>(tm, nlines, slot, sink); }
+    };
+    for (int i = 0; i < 3; ++i) launch();
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0));
+    for (int i = 0; i < 10; ++i) launch();
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    printf("PAIR (32-B rows, 1 column x 2 comps per box) nslot=%d: %7.1f us  %7.0f GB/s\n", ns, 1e3 * ms / 10,
+           (double)nlines * slot / (1e6 * ms / 10));
   }
   for (int W : {1, 2, 4, 8}) {
     for (int i = 0; i < 3; ++i) k_ldg<<<nsm * 2, 512>>>(f, L, W, NC, sink);
