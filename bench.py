@@ -44,6 +44,7 @@ ALPHA, BETA = 0.25, 4.0
 SOLVES = [("em", 0.1), ("em", 10.0), ("em", 1000.0), ("em_sub", 0.1), ("em_sub", 10.0), ("em_sub", 1000.0)]
 WORKLOADS = {
     "c2": SOLVES,
+    "c1": [("basic", 10.0)],  # BASELINE configs[0]: 256^2, basic, tol 1e-8 (set_workload)
     "c2-emsub10": [("em_sub", 10.0)],
     "c2-fast": [("em", 0.1), ("em", 10.0), ("em_sub", 0.1), ("em_sub", 10.0)],
     "c5": None,  # BASELINE configs[4]: 256-point complex sigma1 sweep, em_sub, 1024^2 (see run_c5)
@@ -68,6 +69,34 @@ def _ncu_traffic(kernel, it_by_scheme, n):
     tot = sum(it_by_scheme.values())
     bytes_ = sum((per[s]["dram_read"] + per[s]["dram_write"]) * k for s, k in it_by_scheme.items()) / tot
     return bytes_, t.get("source")
+
+
+def _ncu_pipes(kernel, it_by_scheme):
+    """FP64-pipe and issue-slot utilisation of `kernel` in the committed ncu
+    capture (launch-weighted over schemes), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            per = json.load(fh).get("kernels", {}).get(kernel, {})
+    except OSError:
+        return None
+    if not all(s in per and "fp64_pipe" in per[s] for s in it_by_scheme):
+        return None
+    tot = sum(it_by_scheme.values())
+    return {k: sum(per[s][k] * n for s, n in it_by_scheme.items()) / tot for k in ("fp64_pipe", "issue_active")}
+
+
+def _fft_passes(kernel, it_by_scheme):
+    """Length-n transforms per voxel and component done by one launch of a 2-D
+    sweep, launch-weighted over schemes."""
+    em_type = {"em": 1, "em_sub": 1}
+    per = {"sweep1_rows_fwd": lambda s: 2 if s in em_type else 1,
+           "sweep2_cols_gamma": lambda s: 3 if s in em_type else 2,
+           "sweep3_rows_inv": lambda s: 1}.get(kernel)
+    if per is None:
+        return None
+    tot = sum(it_by_scheme.values())
+    return sum(per(s) * n for s, n in it_by_scheme.items()) / tot
 
 
 def _peaks():
@@ -194,15 +223,16 @@ def _oracle_sample(args):
     return int(chi.size) * r.iterations, dt
 
 
-def cpu_baseline(iters: int = 6) -> dict:
+def cpu_baseline(iters: int = 6, sample=(("em", 10.0), ("em_sub", 10.0))) -> dict:
     """Single-core oracle port on a bounded sample of the workload."""
     tot_v, tot_t = 0, 0.0
-    for scheme, s1 in (("em", 10.0), ("em_sub", 10.0)):
+    for scheme, s1 in sample:
         v, t = _oracle_sample((scheme, s1, N_GRID, iters))
         tot_v += v
         tot_t += t
     return {"value": tot_v / tot_t, "unit": "voxel-iterations/s", "cores": 1, "kind": "port",
-            "sample": f"em and em_sub at sigma1=10 on {N_GRID}^2, {iters} iterations each "
+            "sample": f"{len(sample)} solves (" + ", ".join(f"{sch} at sigma1={v:g}" for sch, v in dict.fromkeys(sample))
+                      + f") on {N_GRID}^2, {iters} iterations each "
                       f"(tol=1e-300 so every iteration runs), oracle/fftcond_oracle.py (numpy pocketfft, "
                       f"bit-identical to the reference loops), {tot_t:.1f} s of CPU work"}
 
@@ -260,8 +290,23 @@ def run_reference(a):
     return 0
 
 
+def set_workload(name):
+    """c1 (BASELINE configs[0]) runs the c2 machinery on its own grid and tolerance."""
+    global N_GRID, TOL, MAX_ITERS
+    if name == "c1":
+        N_GRID, TOL, MAX_ITERS = 256, 1e-8, 1000
+
+
 def _config(a):
     solves = WORKLOADS[a.workload]
+    if a.workload == "c1":
+        return {"workload": f"BASELINE configs[0]: {N_GRID}x{N_GRID} square array f=0.25, basic@sigma1=10, "
+                            f"sigma0=(sigma1+1)/2, tol={TOL:g}",
+                "grid": [N_GRID, N_GRID], "schemes": ["basic"], "sigma1": [10.0], "tol": TOL,
+                "max_iters": MAX_ITERS,
+                "l2": "working set (~8 MB) is L2-resident by nature; L2 flushed (256 MB write) before every "
+                      "timed step, outside that step's CUDA events",
+                "parallelism": "replicas" if _dist()[0] > 1 else "single GPU"}
     return {"workload": f"BASELINE configs[1]: {N_GRID}x{N_GRID} square array f=0.25, "
                         + ", ".join(f"{s}@sigma1={v:g}" for s, v in solves) + f", tol={TOL:g}",
             "grid": [N_GRID, N_GRID], "schemes": [s for s, _ in solves], "sigma1": [v for _, v in solves],
@@ -331,17 +376,31 @@ def run_ours(a):
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = native.lib().fftc_launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
     results = None
-    for _ in range(a.steps):
-        results = step_device()
-    e1.record(stream)
+    if a.workload == "c1":
+        # L2-resident workload: flush L2 before every step, time each step alone
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        pairs = []
+        for _ in range(a.steps):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            results = step_device()
+            e1.record(stream)
+            pairs.append((e0, e1))
+    else:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            results = step_device()
+        e1.record(stream)
+        pairs = [(e0, e1)]
     barrier()
     launches = native.lib().fftc_launch_count() - launches0
     clk = clocks.stop()
-    ms_total = e0.elapsed_time(e1)
+    ms_total = sum(b.elapsed_time(c) for b, c in pairs)
     ms = ms_total / a.steps
     vox = sum(N_GRID * N_GRID * r.iterations for r in results)
     # ---- one profiled step: per-kernel CUDA-event durations for the roofline ----
@@ -401,7 +460,12 @@ def run_ours(a):
                 "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "bytes_per_launch": bpv * N, "avg_launch_ms": per_launch_ms, "launches": nl,
                 "share_of_step": tms / prof_ms if prof_ms > 0 else None,
-                "timing": "CUDA events around every launch of one profiled step (one iteration per sync)"}
+                "timing": "CUDA events around every launch of one profiled step (one iteration per sync)",
+                # the sweeps are bound by their transforms, not by HBM: FFT
+                # points per second of the dominant kernel and its pipe utilisation in the ncu capture
+                "fft_passes_per_voxel_component": _fft_passes(name, it_by_scheme),
+                "fft_gpoints_per_s": (_fft_passes(name, it_by_scheme) or 0.0) * 2 * N / (per_launch_ms / 1e3) / 1e9,
+                "ncu_pipes": _ncu_pipes(name, it_by_scheme)}
     survey_b = sum(_survey_bytes(s, 2, frac) * n for s, n in it_by_scheme.items()) / tot_it
     ours_b = sum(sum(_bytes_per_voxel(s, 2, frac).values()) * n for s, n in it_by_scheme.items()) / tot_it
     iter_roof = {"bytes_per_voxel_iter_survey": survey_b, "bytes_per_voxel_iter_schedule": ours_b,
@@ -426,7 +490,8 @@ def run_ours(a):
                     "sigma_star": [r.sigma_star.real, r.sigma_star.imag]} for (s, v), r in zip(solves, results)],
     }
     if ws == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(a.cpu_iters)
+        line["cpu_baseline"] = (cpu_baseline(62, (("basic", 10.0),) * 30) if a.workload == "c1"
+                                else cpu_baseline(a.cpu_iters))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -622,6 +687,7 @@ def main():
     ap.add_argument("--c5-points", type=int, default=256)
     ap.add_argument("--n3d", type=int, default=0, help="c3/c4 grid side (default: the BASELINE size)")
     a = ap.parse_args()
+    set_workload(a.workload)
     if a.workload == "c5" and a.impl == "ours":
         return run_c5(a)
     if a.workload in ("c3", "c4") and a.impl == "ours":
