@@ -605,8 +605,9 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   const size_t partial_cap = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   char* ws = nullptr;
   const bool two_work = (scheme == FFTC_EM || scheme == FFTC_EM_SUB);  // B holds the flux transform
+  const bool chi_perm = !general && nx >= 16;  // thread-blocked chi rows for the TMA row sweeps
   const size_t ws_bytes = fld * (nslots + (two_work ? 2 : 1)) + sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring +
-                          sizeof(DevState) + sizeof(int2) * (size_t)ny * nz + 8192;
+                          sizeof(DevState) + sizeof(int2) * (size_t)ny * nz + (chi_perm ? (size_t)N + 256 : 0) + 8192;
   CK(cudaMallocAsync((void**)&ws, ws_bytes, s));
   size_t o = 0;
   auto carve = [&](size_t bytes) {
@@ -622,6 +623,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   a.hist_cap = hist_ring;
   a.st = (DevState*)carve(sizeof(DevState));
   a.row_ext = (const int2*)carve(sizeof(int2) * (size_t)ny * nz);
+  a.chiT = chi_perm ? (const uint8_t*)carve((size_t)N) : nullptr;
   a.dbg = getenv("FFTC_PHASE") ? (unsigned long long*)carve(sizeof(unsigned long long) * 8) : nullptr;
   if (a.dbg) CK(cudaMemsetAsync(a.dbg, 0, sizeof(unsigned long long) * 8, s));
   a.outE = (double2*)E;
@@ -671,6 +673,12 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       unsigned g = (unsigned)std::min<long long>((rows + 7) / 8, (long long)R.num_sms * 8);
       void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
       if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) break;
+      if (chi_perm) {
+        const long long chunks = rows * (nx / 16);
+        unsigned gp = (unsigned)std::min<long long>((chunks + 255) / 256, (long long)R.num_sms * 16);
+        void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT};
+        if ((rc = Lc.raw((const void*)k_chi_perm16, gp, 256, 0, pa, K_INIT))) break;
+      }
     }
     switch (scheme) {
       case FFTC_BASIC: rc = launch_elementwise(k_init<BASIC>, Lc, (long long)d * N, a, K_INIT); break;
@@ -1397,7 +1405,7 @@ int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, 
   const int hist_cap = (int)std::max<int64_t>(pr->max_iters, 16);
   const size_t pc = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   const size_t bytes = fld * nslots + sizeof(double) * pc + sizeof(double) * 3 * hist_cap + sizeof(DevState) +
-                       sizeof(int2) * (size_t)ny * sd->nzl + sizeof(double) * 8 + 8192;
+                       sizeof(int2) * (size_t)ny * sd->nzl + sizeof(double) * 8 + (size_t)N_l + 256 + 8192;
   if (cudaMalloc((void**)&sl->ws, bytes) != cudaSuccess) {
     g_err = "slab: workspace allocation failed";
     delete sl;
@@ -1415,6 +1423,7 @@ int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, 
   a.hist_cap = hist_cap;
   a.st = (DevState*)carve(sizeof(DevState));
   a.row_ext = (const int2*)carve(sizeof(int2) * (size_t)ny * sd->nzl);
+  a.chiT = nx >= 16 ? (const uint8_t*)carve((size_t)N_l) : nullptr;  // thread-blocked chi rows (TMA row sweeps)
   sl->tot_dev = (double*)carve(sizeof(double) * 8);
   a.A = (double2*)Az;
   a.B = sl->em_type ? (double2*)Bz : (double2*)Az;
@@ -1488,6 +1497,12 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
       unsigned g = (unsigned)std::min<long long>((rows + 7) / 8, (long long)R.num_sms * 8);
       void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
       if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) return rc;
+      if (a.chiT) {
+        const long long chunks = rows * (a.nx / 16);
+        unsigned gp = (unsigned)std::min<long long>((chunks + 255) / 256, (long long)R.num_sms * 16);
+        void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT};
+        if ((rc = Lc.raw((const void*)k_chi_perm16, gp, 256, 0, pa, K_INIT))) return rc;
+      }
       switch (sl->scheme) {
         case FFTC_BASIC: rc = launch_elementwise(k_init<BASIC>, Lc, (long long)d * a.N, a, K_INIT); break;
         case FFTC_EM: rc = launch_elementwise(k_init<EM>, Lc, (long long)d * a.N, a, K_INIT); break;

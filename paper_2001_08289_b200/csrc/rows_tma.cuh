@@ -72,7 +72,17 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
       if constexpr (K::ST_ROWS > 1) bulk_g2s(stage + K::ST_OFF + K::LP + x0, a.X[2] + off + x0, nb, bar);
     }
   }
-  bulk_g2s(stage + K::CHI_OFF, a.chi + (size_t)row * L, (unsigned)L, bar);
+  bulk_g2s(stage + K::CHI_OFF, a.chiT + (size_t)row * L, (unsigned)L, bar);  // thread-blocked chi row
+}
+
+// a thread's 16 phase flags (chiT row bytes t*16 .. t*16+15, element i = byte i)
+struct ChiBytes16 {
+  uint32_t w[4];
+  __device__ __forceinline__ bool in1(int i) const { return ((w[i >> 2] >> ((i & 3) << 3)) & 0xffu) != 0u; }
+};
+__device__ __forceinline__ ChiBytes16 load_chi16(const uint8_t* chi_s, int t) {
+  const uint4 c = *reinterpret_cast<const uint4*>(chi_s + 16 * t);
+  return ChiBytes16{{c.x, c.y, c.z, c.w}};
 }
 
 template <int S, int SW, int L>
@@ -105,7 +115,7 @@ __device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, int line,
 // exchange buffer; each position is read and rewritten by one thread only).
 template <int H, int L, int E, int NQ>
 __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)[1][E], const double2* st,
-                                                     const uint8_t* chi_s, double2* other, int t, int c, size_t off,
+                                                     const ChiBytes16& cb, double2* other, int t, int c, size_t off,
                                                      double2 dl, double (&acc)[NQ]) {
   // S/T loads (phase 1 only, L2-prefetched) in batches of NB issued ahead of
   // the batch's staging stores; interleaved with them each would wait one latency
@@ -117,7 +127,7 @@ __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)
     for (int u = 0; u < NB; ++u) {
       const int x = pos_first<L, E>(false, t, H * (E / 2) + k0 + u);
       sv[u] = tv[u] = czero();
-      if (chi_s[x] != 0) {
+      if (cb.in1(H * (E / 2) + k0 + u)) {
         sv[u] = a.X[1][off + x];
         tv[u] = a.X[2][off + x];
       }
@@ -126,7 +136,7 @@ __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)
     for (int u = 0; u < NB; ++u) {
       const int i = H * (E / 2) + k0 + u;
       const int x = pos_first<L, E>(false, t, i);
-      const bool in1 = chi_s[x] != 0;
+      const bool in1 = cb.in1(i);
       const double2 q = st[x];
       const AugFlux f = apply_A(a, in1, q, sv[u], tv[u]);
       double2 jq, js;
@@ -185,6 +195,7 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
     const double2 dl = sdelta[c];
     double2* st = smem + s * K::STAGE;
     const uint8_t* chi_s = reinterpret_cast<const uint8_t*>(st + K::CHI_OFF);
+    static_assert(E == 16, "the thread-blocked chi rows (k_chi_perm16) hold 16 flags per thread");
     if (pf) {
       const int2 ext = ext_next;
       const int l2 = line + 2 * (int)gridDim.x;
@@ -192,18 +203,19 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
       rows_tma_prefetch_slots<S, SW, L>(a, line + (int)gridDim.x, lines, rows, ext);
     }
     mbar_wait(&bars[s], parity);
+    const ChiBytes16 cb = load_chi16(chi_s, t);
     double2 v[1][E];
     constexpr bool SPLIT = (SW == 1 && S == EM_SUB && CH == 2 && K::ST_ROWS == 0);
     if constexpr (SPLIT) {
       // ---- prologue, each element once (see em_sub_prologue_half) ----
-      if (ch == 0) em_sub_prologue_half<0, L, E, NQ>(a, v, st, chi_s, xbuf, t, c, off, dl, acc);
-      else em_sub_prologue_half<1, L, E, NQ>(a, v, st, chi_s, st, t, c, off, dl, acc);
+      if (ch == 0) em_sub_prologue_half<0, L, E, NQ>(a, v, st, cb, xbuf, t, c, off, dl, acc);
+      else em_sub_prologue_half<1, L, E, NQ>(a, v, st, cb, st, t, c, off, dl, acc);
     } else if constexpr (SW == 1) {
       // ---- prologue: fields to transform (solvers.py:303-311 / :398-420) ----
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int x = pos_first<L, E>(false, t, i);
-        const bool in1 = chi_s[x] != 0;
+        const bool in1 = cb.in1(i);
         const double2 q = st[x];
         if constexpr (S == BASIC) {
           const double2 j = cmul(sigma_at(a, in1), cadd(q, dl));
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowT
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
           const int x = pos_last<L, E>(true, t, b0 + u);
-          in1v[u] = chi_s[x] != 0;
+          in1v[u] = cb.in1(b0 + u);
           qv[u] = sv[u] = tv[u] = czero();
           if constexpr (S == BASIC_SUB) {
             if (in1v[u]) sv[u] = a.X[1][off + x];

@@ -65,6 +65,10 @@ struct Args {
   long long N;
   const uint8_t* chi;
   const int2* row_ext;  // per row (z,y): [first, last+1) x-extent of phase 1 (empty: x0 >= x1)
+  // chi rows permuted for the TMA row sweeps (16 elements per thread): row
+  // byte t*16 + i holds chi[t + i*nx/16], so a thread's 16 phase flags are one
+  // 16-byte shared-memory load (k_chi_perm16)
+  const uint8_t* chiT;
   double2* X[3];  // state slots: e_raw | Q_raw, S_raw, T_raw
   double2* A;     // work field 0 (d*N)
   double2* B;     // work field 1 (d*N)
@@ -730,6 +734,27 @@ static __global__ void __launch_bounds__(256) k_row_extent(const uint8_t* __rest
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
     if (lane == 0) ext[r] = make_int2(lo, hi + 1);
+  }
+}
+
+// chi rows -> the thread-blocked order of the row sweeps (Args::chiT): one
+// thread per 16-byte output chunk (row r, thread slot t) gathers the 16 bytes
+// chi[r][t + i*T], i = 0..15, T = nx/16 (consecutive t read consecutive bytes)
+static __global__ void __launch_bounds__(256) k_chi_perm16(const uint8_t* __restrict__ chi, int nx, long long rows,
+                                                          uint8_t* __restrict__ out) {
+  const int T = nx >> 4;
+  const long long n = rows * T;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long r = idx / T;
+    const int t = (int)(idx - r * T);
+    const uint8_t* src = chi + (size_t)r * nx + t;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = (uint32_t)(src[(4 * k) * T] != 0) | ((uint32_t)(src[(4 * k + 1) * T] != 0) << 8) |
+             ((uint32_t)(src[(4 * k + 2) * T] != 0) << 16) | ((uint32_t)(src[(4 * k + 3) * T] != 0) << 24);
+    *reinterpret_cast<uint4*>(out + (size_t)r * nx + 16 * t) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
