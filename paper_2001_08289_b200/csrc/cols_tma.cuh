@@ -108,8 +108,9 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
   const int comp = (ht >> CB) & 1, t = (ht & ((1 << CB) - 1)) | ((ht >> (CB + 1)) << CB);
   const HalfSync hsync{1 + half, K::HALF};
   const int nfields = (MODE == MID_EM) ? 2 : 1;
-  const long long lines = (long long)a.nx * nfields;
-  const long long nmine = blockIdx.x < lines ? (lines - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // 32-bit line bookkeeping (nx <= 4096): the loop state stays in registers
+  const int lines = a.nx * nfields;
+  const int nmine = (int)blockIdx.x < lines ? (lines - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < K::NSLOT; ++s) {
       mbar_init(&bars[s], 1);
@@ -120,9 +121,9 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
   __syncthreads();
   if (threadIdx.x == 0)
     for (int s = 0; s < K::NSLOT && s < nmine; ++s) {
-      const long long line = blockIdx.x + (long long)s * gridDim.x;
-      const int f = (int)(line / a.nx);
-      cols_tma_issue<L>(f == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], (int)(line - (long long)f * a.nx));
+      const int line = (int)blockIdx.x + s * (int)gridDim.x;
+      const int f = line / a.nx;
+      cols_tma_issue<L>(f == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], line - f * a.nx);
     }
   double2* tws = smem + K::NSLOT * K::SLOT;
   for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[1][i]);
@@ -132,11 +133,11 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
 #ifdef FFTC_PHASE_TIMING
   long long tph_ = clock64();
 #endif
-  for (long long k = half; k < nmine; k += 2) {
-    const int s = (int)(k % K::NSLOT);
-    const long long line = blockIdx.x + k * gridDim.x;
-    const int f = (int)(line / a.nx);
-    const int x = (int)(line - (long long)f * a.nx);
+  for (int k = half; k < nmine; k += 2) {
+    const int s = k % K::NSLOT;
+    const int line = (int)blockIdx.x + k * (int)gridDim.x;
+    const int f = line / a.nx;
+    const int x = line - f * a.nx;
     double2* slot = smem + s * K::SLOT;
     const double2* inb = slot + comp * L;  // TMA landing layout [comp][y]
     // exchange buffers: component c at c*CB, component 1 skewed by 4 slots
@@ -200,9 +201,9 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
     if (ht == 0) mbar_arrive(&cbars[s]);  // after the hsync above: every thread of this half is done with slot s
     if (ht == 0 && k + K::NSLOT < nmine) {
       fence_proxy_async();
-      const long long nl = line + (long long)K::NSLOT * gridDim.x;
-      const int nf = (int)(nl / a.nx);
-      cols_tma_issue<L>(nf == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], (int)(nl - (long long)nf * a.nx));
+      const int nl = line + K::NSLOT * (int)gridDim.x;
+      const int nf = nl / a.nx;
+      cols_tma_issue<L>(nf == 0 ? &tmA : &tmB, smem + s * K::SLOT, &bars[s], nl - nf * a.nx);
       PHASE_MARK(7);
     }
   }
