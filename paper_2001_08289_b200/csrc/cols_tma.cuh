@@ -33,6 +33,10 @@ struct ColTma {
   static_assert(SMEM <= 232448 - 64, "column kernel exceeds the 227 KB dynamic shared memory limit");
   static constexpr int BOXR = L < 256 ? L : 256;  // rows per TMA box
   static constexpr unsigned TX = (unsigned)(2 * L * sizeof(double2));
+  // one CTA per SM at L = 2048 (the ring fills shared memory); shorter
+  // columns fit several CTAs, up to 16 warps per SM
+  static constexpr int MINB_FILL = (232448 / (SMEM + 2048)) < (512 / THREADS) ? (232448 / (SMEM + 2048)) : (512 / THREADS);
+  static constexpr int MINB = MINB_FILL > 1 ? MINB_FILL : 1;
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
@@ -85,7 +89,7 @@ __device__ __forceinline__ void cols_tma_issue(const CUtensorMap* tm, double2* s
 #endif
 
 template <int MODE, int L>
-__global__ void __launch_bounds__(ColTma<L>::THREADS, 1)
+__global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
     k_mid2_tma(Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
   using K = ColTma<L>;
   constexpr int E = K::E;

@@ -43,6 +43,14 @@ struct RowTma {
   static constexpr int XBUF = (CH == 2 && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
   static constexpr int SMEM = (NSTAGE * STAGE + XBUF) * (int)sizeof(double2);
   static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + L);
+  // resident CTAs per SM the register budget is sized for: the tuned values
+  // for sweep 3 and at L >= 2048; shorter sweep-1 rows (fewer threads per
+  // line) fill the SM up to 16 warps or the shared-memory limit, whichever
+  // comes first (1024^2 em_sub sweep 1 44.3 -> 41.0 us; sweep 3 measured
+  // 23.2 -> 24.3 us for em that way, so it keeps 3)
+  static constexpr int MINB_TUNED = SW == 3 ? 3 : (ST_ROWS ? 1 : 2);
+  static constexpr int MINB_FILL = (232448 / (SMEM + 1024)) < (512 / THREADS) ? (232448 / (SMEM + 1024)) : (512 / THREADS);
+  static constexpr int MINB = (L >= 2048 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1);
 };
 
 template <int S, int SW, int L>
@@ -151,7 +159,7 @@ __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)
 }
 
 template <int S, int SW, int L>
-__global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, SW == 3 ? 3 : (RowTma<S, SW, L>::ST_ROWS ? 1 : 2)) k_rows_tma(Args a) {
+__global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::MINB) k_rows_tma(Args a) {
   using K = RowTma<S, SW, L>;
   constexpr int E = K::E, T = K::T, CH = K::CH;
   constexpr int NQ = (SW == 1) ? Sweep1Traits<S>::NQ : 6;
