@@ -528,6 +528,8 @@ def run_c5(a):
     _solve_local_gpu(pm, mine[:2])  # warm up
     stream = torch.cuda.current_stream()
     times, recs = [], None
+    clocks = ClockSampler(local)
+    clocks.start()
     launches0 = native.lib().fftc_launch_count()
     for step in range(max(1, a.steps)):
         if ws > 1:
@@ -543,18 +545,56 @@ def run_c5(a):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     launches = native.lib().fftc_launch_count() - launches0
+    clk = clocks.stop()
     ms = sum(times) / len(times)
+    # end to end: a fresh host phase map per step (chi host->device inside the
+    # timed region, histories device->host), through the public sweep API
+    chi_host = np.asarray(pm.chi)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    t_wall = time.perf_counter()
+    f0.record(stream)
+    recs_e2e = solve_sweep(fb.PhaseMap(chi_host), cfgs)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = max(f0.elapsed_time(f1), 1e3 * (time.perf_counter() - t_wall))
     if ws > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms, ms_e2e], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t[0])
+        ms, ms_e2e = float(t[0]), float(t[1])
     vox = sum(n * n * r["iterations"] for r in recs)
     value = vox / (ms / 1e3)
+    e2e_value = sum(n * n * r["iterations"] for r in recs_e2e) / (ms_e2e / 1e3)
     hbm, src = _peaks()
     V = 32.0
     bpv = 8 * V + 7 * 0.25 * V + 2
+    # roofline of the dominant kernel: per-launch CUDA events over a few points
+    # solved one after another (profiling mode: one iteration per sync)
+    from paper_2001_08289_b200.solver import _solve_aug
+
+    native.profile(True)
+    for c in cfgs[:4]:
+        _solve_aug(pm, c, True, want_fields=False)
+    torch.cuda.synchronize()
+    kstats = native.kernel_stats()
+    native.profile(False)
+    frac = float(np.asarray(pm.chi).mean())
+    roof = None
+    if kstats:
+        name, (nl, tms) = max(((k, v) for k, v in kstats.items() if k.startswith("sweep")), key=lambda kv: kv[1][1])
+        per_launch_ms = tms / nl
+        bl = _bytes_per_voxel("em_sub", 2, frac)[name] * n * n
+        achieved = bl / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_source": src, "bytes_per_launch": bl,
+                "avg_launch_ms": per_launch_ms, "launches": nl,
+                "fft_gpoints_per_s": _fft_passes(name, {"em_sub": 1}) * 2 * n * n / (per_launch_ms / 1e3) / 1e9,
+                "timing": "CUDA events around every launch of 4 points solved in turn (one iteration per sync)"}
     conv = sum(1 for r in recs if r["status"].value == "Converged")
     line = {"metric": "fp64 voxel-iterations/sec of the FFT iteration", "value": value,
             "unit": "voxel-iterations/s", "n_gpus": ws, "steps": len(times), "warmup": 1, "ms_per_step": ms,
@@ -564,8 +604,20 @@ def run_c5(a):
                                    "max_iters 1000", "parallelism": f"points sharded over {ws} GPU(s)"},
             "iteration_roofline": {"bytes_per_voxel_iter_schedule": bpv, "frac_schedule_bytes": value * bpv / 1e9 / hbm / ws,
                                    "peak_gbs": hbm, "peak_source": src},
-            "gpu_launches": int(launches * ws), "points_converged": conv, "points_total": len(recs),
+            "roofline": roof,
+            "e2e": {"value": e2e_value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": n * n,
+                    "d2h_bytes_per_step": 24 * sum(r["iterations"] for r in recs_e2e) + 256 * len(recs_e2e)},
+            "gpu_launches": int(launches * ws), "clocks": clk, "points_converged": conv, "points_total": len(recs),
             "total_iterations": sum(r["iterations"] for r in recs)}
+    if ws == 1 and not a.no_cpu_baseline:
+        tot_v, tot_t = 0, 0.0
+        for p_ in pts[:2]:
+            v_, t_ = _oracle_sample(("em_sub", p_, n, a.cpu_iters))
+            tot_v += v_
+            tot_t += t_
+        line["cpu_baseline"] = {"value": tot_v / tot_t, "unit": "voxel-iterations/s", "cores": 1, "kind": "port",
+                                "sample": f"2 of the sweep's sigma1 points, em_sub on {n}^2, {a.cpu_iters} iterations each "
+                                          f"(tol=1e-300), oracle/fftcond_oracle.py, {tot_t:.1f} s of CPU work"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
