@@ -44,13 +44,14 @@ struct RowTma {
   static constexpr int SMEM = (NSTAGE * STAGE + XBUF) * (int)sizeof(double2);
   static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + L);
   // resident CTAs per SM the register budget is sized for: the tuned values
-  // for sweep 3 and at L >= 2048; shorter sweep-1 rows (fewer threads per
-  // line) fill the SM up to 16 warps or the shared-memory limit, whichever
-  // comes first (1024^2 em_sub sweep 1 44.3 -> 41.0 us; sweep 3 measured
-  // 23.2 -> 24.3 us for em that way, so it keeps 3)
+  // for sweep 3 and at L != 1024; sweep-1 rows of 1024 (64 threads per
+  // channel) fill the SM up to 16 warps or the shared-memory limit, whichever
+  // comes first (1024^2 em_sub sweep 1 44.3 -> 41.0 us; the same rule cost
+  // em sweep 3 at 1024 23.2 -> 24.3 us and em_sub sweep 1 at 512^3 5.37 ->
+  // 5.78 ms, so those keep the tuned values)
   static constexpr int MINB_TUNED = SW == 3 ? 3 : (ST_ROWS ? 1 : 2);
   static constexpr int MINB_FILL = (232448 / (SMEM + 1024)) < (512 / THREADS) ? (232448 / (SMEM + 1024)) : (512 / THREADS);
-  static constexpr int MINB = (L >= 2048 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1);
+  static constexpr int MINB = (L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1);
 };
 
 template <int S, int SW, int L>
