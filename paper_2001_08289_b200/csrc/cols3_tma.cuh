@@ -86,15 +86,17 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
   if (!a.op_mode && a.st->stopped) return;
   const int w = threadIdx.x % W, t = (threadIdx.x / W) % T, comp = threadIdx.x / (W * T);
   const int nstrips = a.nx / W;
-  const long long per_field = (long long)g.nouter * nstrips;
-  const long long tiles = per_field * g.nfields;
-  const long long nmine = blockIdx.x < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto coords = [&](long long k, int& f, int& o, int& x0) {
-    const long long tile = blockIdx.x + k * gridDim.x;
-    f = (int)(tile / per_field);
-    const long long r = tile - (long long)f * per_field;
-    o = (int)(r / nstrips);
-    x0 = (int)(r - (long long)o * nstrips) * W;
+  // 32-bit tile bookkeeping (at most 2 * 4096 * 4096 / W tiles): 64-bit loop
+  // state spilled in the 2-D projection sweep, keep it out of the registers here
+  const int per_field = g.nouter * nstrips;
+  const int tiles = per_field * g.nfields;
+  const int nmine = (int)blockIdx.x < tiles ? (tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  auto coords = [&](int k, int& f, int& o, int& x0) {
+    const int tile = (int)blockIdx.x + k * (int)gridDim.x;
+    f = tile / per_field;
+    const int r = tile - f * per_field;
+    o = r / nstrips;
+    x0 = (r - o * nstrips) * W;
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < K::NSLOT; ++s) mbar_init(&bars[s], 1);
@@ -112,8 +114,8 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
   __syncthreads();
   const SmemTw tw{tws};
   double acc = 0.0;
-  for (long long k = 0; k < nmine; ++k) {
-    const int s = (int)(k % K::NSLOT);
+  for (int k = 0; k < nmine; ++k) {
+    const int s = k % K::NSLOT;
     int f, o, x0;
     coords(k, f, o, x0);
     double2* slot = smem + s * K::SLOT;
@@ -124,8 +126,8 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
     __syncthreads();  // every input is in registers: the slot becomes exchange scratch
     if (threadIdx.x == 0 && k + K::NSLOT - 1 < nmine) {
       // tile k+NSLOT-1 into the slot of tile k-1, whose store was committed one tile ago
-      const long long nk = k + K::NSLOT - 1;
-      const int ns = (int)(nk % K::NSLOT);
+      const int nk = k + K::NSLOT - 1;
+      const int ns = nk % K::NSLOT;
       int nf, no, nx0;
       coords(nk, nf, no, nx0);
       col3_issue(nf == 0 ? &tmA : &tmB, smem + ns * K::SLOT, &bars[ns], nx0, col3_outer(g, no), K::TX);
