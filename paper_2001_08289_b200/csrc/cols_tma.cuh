@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
   for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[1][i]);
   __syncthreads();
   const SmemTw twy{tws};
+  const double tdbl = (double)t;  // (ny == L: this kernel's columns span the grid)
   double acc[NQ] = {0.0};
 #ifdef FFTC_PHASE_TIMING
   long long tph_ = clock64();
@@ -160,12 +161,17 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
     fft_line<L, E, 1, false>(v, t, twy, SmemBuf{xbuf, 0}, hsync);
     PHASE_MARK(3);
     const double kx = (double)wavenum(x, a.nx);
+    const double kx2 = kx * kx;
     const bool parseval_only = (MODE == MID_EM) && f == 1;
 #pragma unroll
     for (int i = 0; i < E; ++i) {
-      const double ky = (double)wavenum(pos_last<L, E>(false, t, i), a.ny);
+      // element i sits at y = t + off_i (off_i a multiple of T, fixed at
+      // compile time), so its wave number is t + (off_i or off_i - L): one
+      // add to the thread's converted index instead of a conversion per element
+      const int off = pos_last<L, E>(false, 0, i);
+      const double ky = tdbl + (double)(off >= L / 2 ? off - L : off);
       const double kc = comp ? ky : kx;
-      const double k2 = kx * kx + ky * ky;
+      const double k2 = fma(ky, ky, kx2);
       const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
       const double2 mine = cscale(v[0][i], kc);
       double2 other;
