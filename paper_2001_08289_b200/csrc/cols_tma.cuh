@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
   __syncthreads();
   const SmemTw twy{tws};
   const double tdbl = (double)t;  // (ny == L: this kernel's columns span the grid)
+  const double g2 = 2.0 * a.gscale;
   double acc[NQ] = {0.0};
 #ifdef FFTC_PHASE_TIMING
   long long tph_ = clock64();
@@ -172,19 +173,20 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
       const double ky = tdbl + (double)(off >= L / 2 ? off - L : off);
       const double kc = comp ? ky : kx;
       const double k2 = fma(ky, ky, kx2);
-      const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
+      const double ik2 = (k2 != 0.0) ? inv_k2(k2) : 0.0;
       const double2 mine = cscale(v[0][i], kc);
       double2 other;
       other.x = __shfl_xor_sync(0xffffffffu, mine.x, 1 << CB);
       other.y = __shfl_xor_sync(0xffffffffu, mine.y, 1 << CB);
-      double2 dot = comp ? cadd(other, mine) : cadd(mine, other);  // kx F_x + ky F_y
-      dot = cscale(dot, ik2);
+      const double2 dot = comp ? cadd(other, mine) : cadd(mine, other);  // kx F_x + ky F_y
+      // one real weight per element: (Gamma^ F)_c = w dot, w = k_c |k|^-2 scale
       if (MODE == MID_BASIC || parseval_only) {
-        const double2 g = cscale(dot, kc);
+        const double2 g = cscale(dot, kc * ik2 * a.gscale);
         acc[0] += cabs2(cscale(g, a.inv_n));
         v[0][i] = g;
-      } else {
-        v[0][i] = csub(v[0][i], cscale(dot, 2.0 * kc));
+      } else {  // (I - 2 Gamma^) F
+        const double w = kc * ik2 * g2;
+        v[0][i] = make_double2(fma(-w, dot.x, v[0][i].x), fma(-w, dot.y, v[0][i].y));
       }
     }
     PHASE_MARK(4);
