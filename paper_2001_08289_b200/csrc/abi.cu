@@ -1675,6 +1675,37 @@ int fftc_slab_set_peers(fftc_slab* sl, int32_t world, void* const* Ay, void* con
     g_err = "slab peers: fused transposes need y and z lines of 256..1024 (TMA tile passes)";
     return 3;
   }
+  // z-blocked slabs for the fused mode: the z-slab work fields (rows of the
+  // row sweeps, y lines of the y passes, targets of the z pass's stores) and
+  // the y-slabs (targets of the y forward pass's stores, z lines of the z
+  // pass) keep 2^zs planes of a row adjacent, as the monolithic solve does,
+  // so neither the transposing stores nor the z lines land one 2 MB page per
+  // 32 bytes.  Falls back to the plain layouts when a map does not encode.
+  int zsA = zblock_shift(nx, ny, nzl), zsY = zblock_shift(nx, nyl, nz);
+  {
+    Registry& RR = reg();
+    const LTable& TY = RR.tab[sl->lgy];
+    const LTable& TZ = RR.tab[sl->lgz];
+    const int nf = sl->em_type ? 2 : 1;
+    Col3Pass yf, yi, md;
+    Args ay = sl->mid;
+    ay.ny = (int)nyl;  // the y-slab holds nyl rows of every z plane
+    bool ok = zsA > 0 && zsY > 0 &&
+              col3_pass_zblk(yf, TY.col[KC_FWD3T], a, a.A, sl->em_type ? a.B : nullptr, 1, zsA, nf) &&
+              col3_pass_zblk(yi, TY.col[KC_INV3T], a, a.A, nullptr, 1, zsA, 1) &&
+              col3_pass_zblk(md, TZ.col[sl->em_type ? KC_MID3T_EM : KC_MID3T_BASIC], ay, sl->mid.A,
+                             sl->em_type ? sl->mid.B : nullptr, 2, zsY, nf);
+    if (ok) {
+      md.g.o0 = sl->zg.o0;  // global y of the slab's first row (wave numbers)
+      md.g.on = (int)ny;
+      sl->yfwd3 = yf;
+      sl->yinv3 = yi;
+      sl->mid3 = md;
+      sl->row.zbs = zsA;
+    } else {
+      zsA = zsY = 0;
+    }
+  }
   PeerOut po[2];
   memset(po, 0, sizeof(po));
   for (int q = 0; q < world; ++q) {
@@ -1694,6 +1725,14 @@ int fftc_slab_set_peers(fftc_slab* sl, int32_t world, void* const* Ay, void* con
   po[1].outer_stride = nx;      // y
   po[1].outer0 = sl->zg.o0;     // y0
   po[1].comp_stride = nzl * ny * nx;
+  po[0].zs = zsY;  // y-slab rows: z blocked, the line (y) inside the block row
+  po[0].blk_line = 0;
+  po[0].bn = nyl;
+  po[0].row_len = nx;
+  po[1].zs = zsA;  // z-slab rows: the line (z) blocked
+  po[1].blk_line = 1;
+  po[1].bn = ny;
+  po[1].row_len = nx;
   cudaStream_t s = (cudaStream_t)stream;
   if (!sl->po_dev) CK(cudaMalloc((void**)&sl->po_dev, sizeof(po)));
   CK(cudaMemcpyAsync(sl->po_dev, po, sizeof(po), cudaMemcpyHostToDevice, s));

@@ -170,12 +170,27 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
       if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
       const bool inv_layout = (MODE != COL_FWD);
       const int rq = po->rows_per_rank;
-      const long long base = comp * po->comp_stride + (po->outer0 + o) * po->outer_stride + x0 + w;
+      if (po->zs > 0) {  // z-blocked destination slabs
+        const int zs = po->zs, msk = (1 << zs) - 1;
+        const long long O = po->outer0 + o;
+        const long long cbase = comp * po->comp_stride + x0 + w;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int pos = pos_last<L, E>(inv_layout, t, i);
-        const int q = pos / rq;
-        po->dst[f][q][base + (long long)(pos - q * rq) * po->line_stride] = v[0][i];
+        for (int i = 0; i < E; ++i) {
+          const int pos = pos_last<L, E>(inv_layout, t, i);
+          const int q = pos / rq;
+          const long long p = pos - q * rq;
+          const long long b = po->blk_line ? p : O, u = po->blk_line ? O : p;
+          const long long row = (((b >> zs) * po->bn + u) << zs) | (b & msk);
+          po->dst[f][q][cbase + row * po->row_len] = v[0][i];
+        }
+      } else {
+        const long long base = comp * po->comp_stride + (po->outer0 + o) * po->outer_stride + x0 + w;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int pos = pos_last<L, E>(inv_layout, t, i);
+          const int q = pos / rq;
+          po->dst[f][q][base + (long long)(pos - q * rq) * po->line_stride] = v[0][i];
+        }
       }
       __syncthreads();  // the slot's exchange reads are done before the next tile lands
     } else if (!parseval_only) {

@@ -592,10 +592,16 @@ struct Line3 {
 // outer index o lands in rank q = pos / rows_per_rank at
 //   dst[field][q] + c*comp_stride + (outer0 + o)*outer_stride
 //                 + (pos - q*rows_per_rank)*line_stride + x.
+// With zs > 0 the destination is z-blocked (2^zs planes of a row adjacent,
+// like Args::zbs): row ((b >> zs)*bn + u) << zs | (b & (2^zs - 1)) of length
+// row_len, where (b, u) = (line position, outer) when blk_line, else
+// (outer, line position); address = c*comp_stride + row*row_len + x.
 struct PeerOut {
   double2* dst[2][8];
   int world, rows_per_rank;
   long long line_stride, outer_stride, outer0, comp_stride;
+  int zs, blk_line;
+  long long bn, row_len;
 };
 
 template <int MODE, int L, int E, int W, int C, int G>
