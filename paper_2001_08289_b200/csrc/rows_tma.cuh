@@ -39,9 +39,24 @@ struct RowTma {
   static constexpr int ST_OFF = LP + (X0_ROW ? L : 0);
   static constexpr int CHI_OFF = ST_OFF + ST_ROWS * LP;     // double2 units
   static constexpr int STAGE = CHI_OFF + L / 16;            // chi row = L bytes
-  static constexpr int NSTAGE = ST_ROWS ? FFTC_ST_NSTAGE : 2;
+  // twiddle table copied to shared memory (swizzled, L/2 entries) instead of
+  // read through L1 (~39 KB left beside the stages), paid for with a
+  // single-stage ring; measured at 2048^2 (us): sweep 1 em 116.5 -> 114.8,
+  // em_sub 136.0 -> 135.0; sweep 3 basic 85.8 -> 79.7, basic_sub 114.5 ->
+  // 94.7, em_sub 97.0 -> 93.3, but em 56.6 -> 61.7 (the lightest sweep loses
+  // more from the shallower ring than it gains), so em's sweep 3 keeps two
+  // stages.  FFTC_ROW_SMEMTW=0 switches it off.
+#ifndef FFTC_ROW_SMEMTW
+#define FFTC_ROW_SMEMTW 1
+#endif
+  // (at 1024 em_sub's sweep 3 measured 34.4 -> 36.3 us with it: 2048 and up)
+  static constexpr bool TWS = FFTC_ROW_SMEMTW && L >= 1024 &&
+                              ((SW == 1 && CH == 2 && ST_ROWS == 0) ||
+                               (SW == 3 && (S == BASIC || S == BASIC_SUB)) || (SW == 3 && S == EM_SUB && L >= 2048));
+  static constexpr int NSTAGE = TWS ? 1 : (ST_ROWS ? FFTC_ST_NSTAGE : 2);
   static constexpr int XBUF = (CH == 2 && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
-  static constexpr int SMEM = (NSTAGE * STAGE + XBUF) * (int)sizeof(double2);
+  static constexpr int TWOFF = NSTAGE * STAGE + XBUF;              // double2 units
+  static constexpr int SMEM = (TWOFF + (TWS ? L / 2 : 0)) * (int)sizeof(double2);
   static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + L);
   // resident CTAs per SM the register budget is sized for: the tuned values
   // for sweep 3 and at L != 1024; sweep-1 rows of 1024 (64 threads per
@@ -181,6 +196,8 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
     fence_mbar_init();
   }
   if (threadIdx.x < 3) sdelta[threadIdx.x] = a.st->delta[threadIdx.x];
+  if constexpr (K::TWS)
+    for (int i = threadIdx.x; i < L / 2; i += blockDim.x) smem[K::TWOFF + tw_swz(i)] = __ldg(&a.tw[0][i]);
   // phase-1 extent of the line after next, for the S/T prefetch
   const bool pf = rows_prefetch_slots<S, SW, L>() && threadIdx.x == blockDim.x - 1;
   int2 ext_next = make_int2(0, 0);
@@ -282,9 +299,15 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
       // only its own T threads (named barrier 1 + ch), not the whole CTA
       // (no barrier after the last exchange: the __syncthreads closing the
       // line comes before the buffer is written again)
-      fft_line<L, E, 1, INV, false>(v, t, a.tw[0], SmemBuf{xb, 0}, HalfSync{1 + ch, T});
+      if constexpr (K::TWS)
+        fft_line<L, E, 1, INV, false>(v, t, SmemTw{smem + K::TWOFF}, SmemBuf{xb, 0}, HalfSync{1 + ch, T});
+      else
+        fft_line<L, E, 1, INV, false>(v, t, a.tw[0], SmemBuf{xb, 0}, HalfSync{1 + ch, T});
     } else {
-      fft_line<L, E, 1, INV, false>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
+      if constexpr (K::TWS)
+        fft_line<L, E, 1, INV, false>(v, t, SmemTw{smem + K::TWOFF}, SmemBuf{xb, 0}, SyncAll{});
+      else
+        fft_line<L, E, 1, INV, false>(v, t, a.tw[0], SmemBuf{xb, 0}, SyncAll{});
     }
     if constexpr (SW == 1) {
       const size_t woff = work_off(a, c, row);  // work field row (z-blocked in 3-D)
