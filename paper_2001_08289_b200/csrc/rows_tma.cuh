@@ -42,7 +42,7 @@ struct RowTma {
   // twiddle table copied to shared memory (swizzled, L/2 entries) instead of
   // read through L1 (~39 KB left beside the stages), paid for with a
   // single-stage ring; measured at 2048^2 (us): sweep 1 em 116.5 -> 114.8,
-  // em_sub 136.0 -> 135.0; sweep 3 basic 85.8 -> 79.7, basic_sub 114.5 ->
+  // em_sub 136.0 -> 135.0, basic 73.2 -> 69.5 (1024^3: 20.6 -> 18.5 ms); sweep 3 basic 85.8 -> 79.7, basic_sub 114.5 ->
   // 94.7, em_sub 97.0 -> 93.3, but em 56.6 -> 61.7 (the lightest sweep loses
   // more from the shallower ring than it gains), so em's sweep 3 keeps two
   // stages.  FFTC_ROW_SMEMTW=0 switches it off.
@@ -50,8 +50,10 @@ struct RowTma {
 #define FFTC_ROW_SMEMTW 1
 #endif
   // (at 1024 em_sub's sweep 3 measured 34.4 -> 36.3 us with it: 2048 and up)
+  // (basic_sub's sweep 1 already stages its S row in a single stage; the table
+  // on top measured 80.2 -> 87.8 us, so it keeps the L1 path)
   static constexpr bool TWS = FFTC_ROW_SMEMTW && L >= 1024 &&
-                              ((SW == 1 && CH == 2 && ST_ROWS == 0) ||
+                              ((SW == 1 && ST_ROWS == 0) ||
                                (SW == 3 && (S == BASIC || S == BASIC_SUB)) || (SW == 3 && S == EM_SUB && L >= 2048));
   static constexpr int NSTAGE = TWS ? 1 : (ST_ROWS ? FFTC_ST_NSTAGE : 2);
   static constexpr int XBUF = (CH == 2 && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
