@@ -52,7 +52,10 @@ struct RowTma {
   // (at 1024 em_sub's sweep 3 measured 34.4 -> 36.3 us with it: 2048 and up)
   // (basic_sub's sweep 1 already stages its S row in a single stage; the table
   // on top measured 80.2 -> 87.8 us, so it keeps the L1 path)
-  static constexpr bool TWS = FFTC_ROW_SMEMTW && L >= 1024 &&
+#ifndef FFTC_TWS_MINL
+#define FFTC_TWS_MINL 1024
+#endif
+  static constexpr bool TWS = FFTC_ROW_SMEMTW && L >= FFTC_TWS_MINL &&
                               ((SW == 1 && ST_ROWS == 0) ||
                                (SW == 3 && (S == BASIC || S == BASIC_SUB)) || (SW == 3 && S == EM_SUB && L >= 2048));
   static constexpr int NSTAGE = TWS ? 1 : (ST_ROWS ? FFTC_ST_NSTAGE : 2);
