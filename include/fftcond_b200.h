@@ -129,7 +129,12 @@ void fftc_slab_destroy(fftc_slab* slab);
  * all-to-alls and only orders the phases (a barrier after ROWS_FWD; the
  * all-reduce after MID).  Ay, Az (and By for em / em_sub): `world` device
  * pointers, rank order, peer-accessible from this rank.  Returns 3 when the
- * grid cannot use the fused passes (y and z lines of 256..1024). */
+ * grid cannot use the fused passes (y and z lines of 256..1024).  In this
+ * mode the work buffers are library-private in layout: A_z/B_z and A_y/B_y
+ * switch to the z-blocked layout (2^zs z-planes of a row adjacent, zs chosen
+ * per slab as for the monolithic solve; FFTC_ZBLOCK=0 keeps the plain
+ * layouts), so callers must not read them as (c, z_l, y, x) / (c, y_l, z, x)
+ * after fftc_slab_set_peers. */
 int fftc_slab_set_peers(fftc_slab* slab, int32_t world, void* const* Ay, void* const* By, void* const* Az,
                         void* stream);
 
