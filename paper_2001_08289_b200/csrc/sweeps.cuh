@@ -383,21 +383,39 @@ __global__ void __launch_bounds__(G * Sweep1Traits<S>::C * (L / E), 2) k_sweep1(
     const double2 dl = a.st->delta[c];
     const size_t woff = work_off(a, c, row);  // work field A/B row
     if (t == 0 && ch == 0) prefetch_row_inputs<S, L, false>(a, line + (long long)gridDim.x * G, lines, rows);
-    double2 v[1][E];
+    // gather first: every load of the line is issued before any is used
+    // (written as one loop, the per-element branches kept each chi/X pair
+    // waiting on the previous one -- 16 serial round trips per line)
+    bool in1v[E];
+    double2 xq[E], xs[E], xt[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int x = pos_first<L, E>(false, t, i);
+      in1v[i] = live && chi[x] != 0;
+      xq[i] = live ? a.X[0][off + x] : czero();
+    }
+    if constexpr (S == BASIC_SUB || S == EM_SUB) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int x = pos_first<L, E>(false, t, i);
+        xs[i] = in1v[i] ? a.X[1][off + x] : czero();
+        xt[i] = (S == EM_SUB && in1v[i]) ? a.X[2][off + x] : czero();
+      }
+    }
+    double2 v[1][E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
       if (!live) {
         v[0][i] = czero();
         continue;
       }
-      const bool in1 = chi[x] != 0;
+      const bool in1 = in1v[i];
       if constexpr (S == BASIC) {
-        double2 j = cmul(sigma_at(a, in1), cadd(a.X[0][off + x], dl));  // j = sigma e  (solvers.py:310-311)
+        double2 j = cmul(sigma_at(a, in1), cadd(xq[i], dl));  // j = sigma e  (solvers.py:310-311)
         v[0][i] = j;
         acc_c<NQ>(acc, c, j);
       } else if constexpr (S == EM) {
-        const double2 er = a.X[0][off + x];
+        const double2 er = xq[i];
         if (jchan) {
           const double2 j = cmul(sigma_at(a, in1), cadd(er, dl));  // j = sigma (e_raw + delta)
           v[0][i] = j;
@@ -406,11 +424,8 @@ __global__ void __launch_bounds__(G * Sweep1Traits<S>::C * (L / E), 2) k_sweep1(
           v[0][i] = cmul(in1 ? a.sm1 : a.sm2, er);  // r = (sigma - s0) e_raw  (:303)
         }
       } else {
-        const double2 q = a.X[0][off + x];
-        const double2 s = in1 ? a.X[1][off + x] : czero();
-        double2 tt = czero();
-        if constexpr (S == EM_SUB) tt = in1 ? a.X[2][off + x] : czero();
-        const AugFlux f = apply_A(a, in1, q, s, tt);  // (:412)
+        const double2 q = xq[i];
+        const AugFlux f = apply_A(a, in1, q, xs[i], xt[i]);  // (:412)
         if (jchan) {
           double2 jq, js;
           pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
@@ -466,17 +481,41 @@ __global__ void __launch_bounds__(G*(L / E), 2) k_sweep3(Args a) {
     double2 v[1][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) v[0][i] = live ? a.A[woff + pos_first<L, E>(true, t, i)] : czero();
-    fft_line<L, E, 1, true>(v, t, a.tw[0], buf, SyncAll{});
-    if (!live) continue;
+    // the update's inputs are loaded before the transform so their latency
+    // hides behind it (after it, the state stores kept them serial)
+    bool in1v[E];
+    double2 xq[E], xs[E], xt[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int x = pos_last<L, E>(true, t, i);
-      const bool in1 = chi[x] != 0;
+      in1v[i] = live && chi[x] != 0;
+      xq[i] = (live && (S == BASIC || S == BASIC_SUB)) ? a.X[0][off + x] : czero();
+    }
+    fft_line<L, E, 1, true>(v, t, a.tw[0], buf, SyncAll{});
+    if (!live) continue;
+    // S/T (phase 1 only) after the transform: across it they would spill;
+    // em_sub gathers and updates half a line at a time for the same reason
+    constexpr int CHK = (S == EM_SUB && E > 1) ? E / 2 : E;
+#pragma unroll
+    for (int i0 = 0; i0 < E; i0 += CHK) {
+    if constexpr (S == BASIC_SUB || S == EM_SUB) {
+#pragma unroll
+      for (int i = i0; i < i0 + CHK; ++i) {
+        const int x = pos_last<L, E>(true, t, i);
+        if (S == EM_SUB) xq[i] = in1v[i] ? a.X[0][off + x] : czero();  // read on phase 1 only
+        xs[i] = in1v[i] ? a.X[1][off + x] : czero();
+        xt[i] = (S == EM_SUB && in1v[i]) ? a.X[2][off + x] : czero();
+      }
+    }
+#pragma unroll
+    for (int i = i0; i < i0 + CHK; ++i) {
+      const int x = pos_last<L, E>(true, t, i);
+      const bool in1 = in1v[i];
       const double2 gq = cscale(v[0][i], a.inv_n);  // ifft normalisation 1/N
       double2 qn;
       if constexpr (S == BASIC) {
         // e_raw <- (e_raw + delta) - g / s0      (solvers.py:306)
-        qn = csub(cadd(a.X[0][off + x], dl), cmul(gq, a.inv_s0));
+        qn = csub(cadd(xq[i], dl), cmul(gq, a.inv_s0));
         a.X[0][off + x] = qn;
       } else if constexpr (S == EM) {
         // w = 2 s0 e0 + (I - 2 Gamma) r;  e_raw = w / (sigma + s0)   (:303-308)
@@ -485,11 +524,11 @@ __global__ void __launch_bounds__(G*(L / E), 2) k_sweep3(Args a) {
         a.X[0][off + x] = qn;
       } else if constexpr (S == BASIC_SUB) {
         // Q_raw <- Q - g/s0 ; S_raw <- chi (S - Js/s0)   (:405-406)
-        double2 q = a.X[0][off + x];
+        double2 q = xq[i];
         qn = csub(cadd(q, dl), cmul(gq, a.inv_s0));
         a.X[0][off + x] = qn;
         if (in1) {
-          double2 s = a.X[1][off + x];
+          double2 s = xs[i];
           AugFlux f = apply_A(a, true, q, s, czero());
           double2 jq, js;
           pinned_flux(a, true, f.jq, f.js, dl, jq, js);
@@ -500,7 +539,7 @@ __global__ void __launch_bounds__(G*(L / E), 2) k_sweep3(Args a) {
         double2 wq = cadd(a.two_s0_e0[c], gq);
         double2 ws = czero(), wt = czero();
         if (in1) {
-          double2 q = a.X[0][off + x], s = a.X[1][off + x], tt = a.X[2][off + x];
+          double2 q = xq[i], s = xs[i], tt = xt[i];
           AugFlux f = apply_A(a, true, q, s, tt);
           const double2 rs = csub(f.js, cmul(a.s0, s));  // Rs = Js_raw - s0 S_raw
           ws = make_double2(-rs.x, -rs.y);
@@ -515,6 +554,7 @@ __global__ void __launch_bounds__(G*(L / E), 2) k_sweep3(Args a) {
         }
       }
       acc_c<NQ>(acc, c, qn);
+    }
     }
   }
   double tot[NQ];
