@@ -417,6 +417,8 @@ def run_ours(a):
     # ---- timed: end to end through the public API, host inputs ----
     step_e2e()  # warm the allocator paths of the public API
     barrier()
+    clocks_e2e = ClockSampler(local)  # the e2e steps run last, often at lower power-capped clocks
+    clocks_e2e.start()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     t_wall = time.perf_counter()
@@ -428,6 +430,7 @@ def run_ours(a):
     f1.record(stream)
     barrier()
     t_wall = time.perf_counter() - t_wall
+    clk_e2e = clocks_e2e.stop()
     ms_e2e = max(f0.elapsed_time(f1), 1e3 * t_wall) / a.steps
     e2e_iters = sum(r.iterations for r in e2e_res)
     # max over ranks
@@ -482,7 +485,7 @@ def run_ours(a):
         "config": _config(a),
         "roofline": roof, "iteration_roofline": iter_roof,
         "e2e": {"value": e2e_value, "unit": "voxel-iterations/s", "h2d_bytes_per_step": N,
-                "d2h_bytes_per_step": 24 * e2e_iters + 256 * len(cfgs)},
+                "d2h_bytes_per_step": 24 * e2e_iters + 256 * len(cfgs), "clocks": clk_e2e},
         "gpu_launches": int(launches), "clocks": clk,
         "kernels": {k: {"launches": v[0], "ms_total": v[1], "ms_per_launch": v[1] / max(v[0], 1)}
                     for k, v in kstats.items()},
