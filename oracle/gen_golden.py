@@ -8,7 +8,8 @@ come from the reference (it is 2-D only, geometry.py:33-34); they come from
 ``oracle/fftcond_oracle.py`` and say so in their ``source`` field.
 
 Usage:  python oracle/gen_golden.py <group> [<group> ...] [--jobs N]
-Groups: edge, c1, c2small, c5small, c2full, c5full, 3d, fields, general, big
+Groups: edge, c1, c2small, c5small, c2full, c5full, 3d, fields, general, big,
+        c3red, c4red, c3first, c3full, c4first
 """
 
 from __future__ import annotations
@@ -84,6 +85,11 @@ def _chi(geom):
     if kind == "random3d":
         rng = np.random.default_rng(geom["seed"])
         return rng.random((geom["n"],) * 3) < geom["frac"]
+    if kind == "c4medium":  # BASELINE config-4 recipe (cell.build_random_medium; frozen file at 1024^3)
+        sys.path.insert(0, REPO)
+        from paper_2001_08289_b200 import cell
+
+        return np.asarray(cell.c4_phase_map(geom["n"]).chi)
     raise ValueError(kind)
 
 
@@ -123,6 +129,28 @@ def run_case(case):
         fields = dict(E=E, J=J)
         if aug is not None:
             fields.update(S=aug.S.data, T=aug.T.data)
+    elif case.get("lean"):
+        # bounded-memory threaded restatement, bit-identical to fftcond_oracle
+        # (tests/test_oracle.py::test_lean_oracle_bitwise)
+        from oracle import fftcond_oracle as O
+        from oracle import lean_oracle as LO
+
+        e0 = None if case.get("e0") is None else [complex(*v) for v in case["e0"]]
+        keep = bool(case.get("keep_fields", True))
+        r = LO.solve(chi, case["scheme"], complex(*case["sigma1"]), e0=e0, tol=case["tol"],
+                     max_iters=case["max_iters"], alpha=ALPHA, beta=BETA, keep_fields=keep)
+        hist = [[k, s.real, s.imag, res] for k, s, res in r.history]
+        out = dict(status=r.status, degenerate_flux=bool(r.degenerate_flux),
+                   iterations=r.iterations, sigma_star=cplx(r.sigma_star), history=hist,
+                   source="oracle/lean_oracle.py (bounded-memory form of the d-generic restatement; "
+                          "no 3-D reference exists)")
+        fields = {}
+        if keep:
+            out["mean_E"] = [cplx(v) for v in O.component_means(r.E)]
+            out["mean_J"] = [cplx(v) for v in O.component_means(r.J)]
+            fields = dict(E=r.E, J=r.J)
+            if r.aug is not None:
+                fields.update(S=r.aug[1], T=r.aug[2])
     else:
         from oracle import fftcond_oracle as O
 
@@ -143,6 +171,10 @@ def run_case(case):
     # size-independent field summaries: sum |F|^2 over the grid, per component
     out["field_sumsq"] = {k: [float(np.sum(np.abs(v[c]) ** 2)) for c in range(v.shape[0])]
                           for k, v in fields.items()}
+    if chi.ndim == 3 and chi.shape[0] >= 128:
+        import hashlib
+
+        out["chi_sha256"] = hashlib.sha256(np.packbits(chi.reshape(-1), bitorder="little").tobytes()).hexdigest()
     out["case"] = case
     if case.get("save_fields"):
         path = os.path.join(GOLDEN, "fields", case["name"] + ".npz")
@@ -213,7 +245,7 @@ def groups():
     g["c5small"] = [C(f"c5s_64_p{i:03d}", sq(64), "em_sub", s, tol=1e-8, max_iters=1000)
                     for i, s in enumerate(pts)]
     g["c5full"] = [C(f"c5_1024_p{i:03d}", sq(1024), "em_sub", s, tol=1e-8, max_iters=1000)
-                   for i, s in enumerate(pts[:16])]
+                   for i, s in enumerate(pts)]
 
     three = []
     for sch in ("basic", "em", "basic_sub", "em_sub"):
@@ -233,6 +265,23 @@ def groups():
     for c in three:
         c["force_oracle"] = True
     g["3d"] = three
+
+    # BASELINE configs 3 and 4 at their recipes: full solves on reduced grids
+    # (SURVEY 8c), first iterations at the stated sizes (c3first here,
+    # c4first on the GPU box host: 1024^3 needs ~165 GB)
+    ex = [[1.0, 0.0], [0.0, 0.0], [0.0, 0.0]]
+    ed = [[1 / math.sqrt(3), 0.0]] * 3
+    c3side = lambda n: 2 * int(round(0.63 * n / 2))  # noqa: E731  (nearest even side; 322 at 512)
+    g["c3red"] = [C(f"c3_cube{n}_em_sub", dict(kind="cube", n=n, side=c3side(n)), "em_sub", 100.0, tol=1e-8,
+                    max_iters=20000, e0=ex, lean=True) for n in (128, 256)]
+    g["c4red"] = [C(f"c4_random{n}_{sch}", dict(kind="c4medium", n=n), sch, 50.0, tol=1e-8, max_iters=20000,
+                    e0=ed, lean=True) for n in (128, 256) for sch in ("basic", "em_sub")]
+    g["c3first"] = [C("c3_cube512_em_sub_first4", dict(kind="cube", n=512, side=c3side(512)), "em_sub", 100.0,
+                      tol=1e-8, max_iters=4, e0=ex, lean=True, keep_fields=False)]
+    g["c3full"] = [C("c3_cube512_em_sub", dict(kind="cube", n=512, side=c3side(512)), "em_sub", 100.0,
+                     tol=1e-8, max_iters=20000, e0=ex, lean=True, keep_fields=False)]
+    g["c4first"] = [C("c4_random1024_basic_first3", dict(kind="c4medium", n=1024), "basic", 50.0, tol=1e-8,
+                      max_iters=3, e0=ed, lean=True, keep_fields=False)]
 
     # grids outside the fused transforms' power-of-two lengths (the general
     # path: pointwise kernels around cuFFT); 2-D from the live reference

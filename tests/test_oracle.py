@@ -135,3 +135,39 @@ class TestKnownAnswers3D:
         assert np.abs(g.mean(axis=(1, 2, 3))).max() <= 1e-13
         c = np.ones((3, 8, 8, 8), complex)
         assert np.abs(O.gamma1(c)).max() <= 1e-14
+
+
+@pytest.mark.parametrize("shape,scheme,s1,e0", [
+    ((32, 32), "basic", 50.0, None),
+    ((32, 32), "em_sub", -30.0 + 5.0j, None),
+    ((16, 16, 16), "basic", 50.0, (3 ** -0.5,) * 3),
+    ((16, 16, 16), "em_sub", 100.0, (1.0, 0.0, 0.0)),
+    ((8, 12, 16), "em_sub", 20.0 + 3.0j, (0.6, 0.2j, -0.3)),
+])
+def test_lean_oracle_bitwise(shape, scheme, s1, e0):
+    """oracle/lean_oracle.py (the bounded-memory form used for the 512^3 and
+    1024^3 fixtures) reproduces fftcond_oracle bit for bit: every history
+    record, sigma*, the returned fields and (em_sub) the augmented slots."""
+    from oracle import lean_oracle as LO
+
+    rng = np.random.default_rng(7)
+    chi = O.centred_box(shape[0], shape[0] // 2, len(shape)) if len(set(shape)) == 1 else rng.random(shape) < 0.3
+    a = O.solve(chi, scheme, s1, e0=e0, tol=1e-10, max_iters=150, alpha=ALPHA, beta=BETA)
+    b = LO.solve(chi, scheme, s1, e0=e0, tol=1e-10, max_iters=150, alpha=ALPHA, beta=BETA)
+    assert (a.status, a.iterations) == (b.status, b.iterations)
+    for (ka, sa, ra), (kb, sb, rb) in zip(a.history, b.history):
+        assert (ka, sa, ra) == (kb, sb, rb)
+    assert np.array_equal(a.E, b.E) and np.array_equal(a.J, b.J)
+    if scheme == "em_sub":
+        assert all(np.array_equal(x, y) for x, y in zip(a.aug, b.aug))
+
+
+def test_c4_medium_frozen_digest(tmp_path):
+    """The config-4 recipe is deterministic: a small instance rebuilt twice is
+    identical, and the frozen 1024^3 digest is what c4_phase_map checks."""
+    from paper_2001_08289_b200 import cell
+
+    a = cell.build_random_medium(32, 3, seed=cell.C4_SEED, smoothing=cell.C4_SMOOTHING, fraction=cell.C4_FRACTION)
+    b = cell.c4_phase_map(32, directory=str(tmp_path))
+    assert a == b and abs(float(a.volume_fraction) - 0.30) < 1e-3
+    assert set(cell.C4_CHI_SHA256) == {1024} and len(cell.C4_CHI_SHA256[1024]) == 64
