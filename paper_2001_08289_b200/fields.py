@@ -30,6 +30,23 @@ def _total(values: np.ndarray) -> float:
     return math.fsum(rows.tolist())
 
 
+# Device fields up to this size come back through page-locked memory (torch's
+# caching host allocator keeps the blocks for the next read): ~3x the
+# bandwidth of a pageable copy.  Larger ones (1024^3: 48 GiB each) take the
+# pageable path so the process does not pin a large share of host RAM.
+PINNED_COPY_MAX_BYTES = 8 << 30
+
+
+def _to_host(dev) -> np.ndarray:
+    import torch
+
+    if dev.numel() * dev.element_size() <= PINNED_COPY_MAX_BYTES:
+        host = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+        host.copy_(dev)  # synchronous: the stream is drained when this returns
+        return host.numpy()
+    return dev.cpu().numpy()
+
+
 class VectorField:
     """Complex d-vector samples on a periodic grid, host or device resident."""
 
@@ -53,7 +70,7 @@ class VectorField:
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            self._host = self._dev.cpu().numpy()
+            self._host = _to_host(self._dev)
             self._dev = None
         return self._host
 

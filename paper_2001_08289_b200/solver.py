@@ -263,12 +263,15 @@ def _params(cfg: SolverConfig, d: int) -> native.Params:
 def _result_from(res: native.Result, hist: np.ndarray, d: int, E=None, J=None, aug=None) -> SolveResult:
     n = int(res.iterations)
     aug_field = None
+    E_field = VectorField.from_device(E) if E is not None else None
     if aug is not None:
-        aug_field = AugmentedField(VectorField.from_device(aug[0]), VectorField.from_device(aug[1]),
-                                   VectorField.from_device(aug[2]))
+        Q = VectorField.from_device(aug[0])
+        aug_field = AugmentedField(Q, VectorField.from_device(aug[1]), VectorField.from_device(aug[2]))
+        if E_field is None:
+            E_field = Q  # one field behind both names, like the reference
     return SolveResult(
         sigma_star=complex(res.sigma_star[0], res.sigma_star[1]),
-        E_field=VectorField.from_device(E) if E is not None else None,
+        E_field=E_field,
         J_field=VectorField.from_device(J) if J is not None else None,
         history=ConvergenceHistory.from_array(hist[:n]),
         status=_STATUS[int(res.status)],
@@ -293,10 +296,13 @@ def _run_device(pmap: PhaseMap, cfg: SolverConfig, want_fields: bool = True) -> 
     hist = np.empty((int(cfg.max_iters), 3), dtype=np.float64)
     E = J = aug = None
     if want_fields:
-        E = torch.empty((d,) + grid, dtype=torch.complex128, device="cuda")
         J = torch.empty((d,) + grid, dtype=torch.complex128, device="cuda")
         if cfg.scheme.substituted:
+            # E and aug.Q are one array, as in the reference (solvers.py:435-443
+            # wraps the same fq in both): the library writes Q once
             aug = torch.empty((3, d) + grid, dtype=torch.complex128, device="cuda")
+        else:
+            E = torch.empty((d,) + grid, dtype=torch.complex128, device="cuda")
     res = native.Result()
     stream = torch.cuda.current_stream().cuda_stream
     rc = L.fftc_solve(C.byref(prob), C.byref(par), hist.ctypes.data, hist.shape[0],
