@@ -45,6 +45,8 @@ struct Col3Tma {
   static constexpr int SMEM = (NSLOT * SLOT + L / 2) * (int)sizeof(double2);
   static constexpr int BOXR = L < 256 ? L : 256;
   static constexpr unsigned TX = (unsigned)(NC * W * L * sizeof(double2));
+  // narrow tiles (384 threads) leave room for two CTAs per SM: registers for both
+  static constexpr int MINB = THREADS <= 384 ? 2 : 1;
   static_assert(THREADS <= 1024, "block size");
   static_assert((SLOT * 16) % 128 == 0, "TMA destinations stay 128-B aligned");
   static_assert(SMEM <= 232448 - 512, "shared memory budget");
@@ -74,7 +76,7 @@ __device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2*
 // device memory) instead of back through the slot and a TMA store -- the
 // decomposed solve's transposes fused into the pass that produces the data.
 template <int MODE, int L, bool PEER = false>
-__global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
+__global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
     k_col3_tma(Args a, Line3 g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const PeerOut* __restrict__ po) {
   using K = Col3Tma<L>;
@@ -134,12 +136,15 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
     }
     double2* xb = slot + (comp * W + w) * K::XS;
     const bool parseval_only = (MODE == MID_EM) && f == 1;
-    if constexpr (!INV_ONLY) fft_line<L, E, 1, false>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
+    // (tail barrier only where the projection needs it; the other paths pass
+    // their own barrier before the slot is written again)
+    if constexpr (!INV_ONLY) fft_line<L, E, 1, false, MID>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
     if constexpr (MID) {
       // Gamma projection (spectral_ops.py:124-127), k = (kx, k_outer, k_line)
-      // for the components (x, y, z); k.F^ gathered across the component warps
+      // for the components (x, y, z); k.F^ gathered across the component warps.
+      // (The forward transform's tail barrier already ordered its last
+      // exchange reads before these writes.)
       const double kx = (double)wavenum(x0 + w, a.nx), ko = (double)wavenum(g.o0 + o, g.on);
-      __syncthreads();  // last exchange reads are done before kf overwrites the buffers
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int pos = pos_last<L, E>(false, t, i);
@@ -147,24 +152,42 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
         slot[(comp * L + pos) * W + w] = cscale(v[0][i], kc);
       }
       __syncthreads();
+      if (parseval_only) {
+        // flux field: only sum_k |Gamma^ j^|^2 / N^2 = sum_k |k.j^|^2 / (|k|^2 N^2)
+        // (Parseval, solvers.py:427-430) -- one evaluation per mode, the
+        // modes of a thread's E elements dealt round robin over the three
+        // component threads that hold them: sum_c |k_c d ik2 / N|^2
+        // = |d ik2 / N|^2 |k|^2 with d = k.F^ and ik2 = scale / |k|^2.
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int pos = pos_last<L, E>(false, t, i);
-        const double kl = (double)wavenum(pos, L);
-        const double kc = comp == 0 ? kx : (comp == 1 ? ko : kl);
-        const double k2 = kx * kx + ko * ko + kl * kl;
-        const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
-        double2 dot = cadd(cadd(slot[pos * W + w], slot[(L + pos) * W + w]), slot[(2 * L + pos) * W + w]);
-        dot = cscale(dot, ik2);
-        if (MODE == MID_BASIC || parseval_only) {
-          const double2 gc = cscale(dot, kc);
-          acc += cabs2(cscale(gc, a.inv_n));  // Parseval on the 1/N-scaled mode
-          v[0][i] = gc;
-        } else {
-          v[0][i] = csub(v[0][i], cscale(dot, 2.0 * kc));
+        for (int i = 0; i < E; ++i) {
+          if (i % 3 != comp) continue;
+          const int pos = pos_last<L, E>(false, t, i);
+          const double kl = (double)wavenum(pos, L);
+          const double k2 = kx * kx + ko * ko + kl * kl;
+          const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
+          const double2 d = cadd(cadd(slot[pos * W + w], slot[(L + pos) * W + w]), slot[(2 * L + pos) * W + w]);
+          acc += cabs2(cscale(d, ik2 * a.inv_n)) * k2;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int pos = pos_last<L, E>(false, t, i);
+          const double kl = (double)wavenum(pos, L);
+          const double kc = comp == 0 ? kx : (comp == 1 ? ko : kl);
+          const double k2 = kx * kx + ko * ko + kl * kl;
+          const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
+          double2 dot = cadd(cadd(slot[pos * W + w], slot[(L + pos) * W + w]), slot[(2 * L + pos) * W + w]);
+          dot = cscale(dot, ik2);
+          if (MODE == MID_BASIC) {
+            const double2 gc = cscale(dot, kc);
+            acc += cabs2(cscale(gc, a.inv_n));  // Parseval on the 1/N-scaled mode
+            v[0][i] = gc;
+          } else {
+            v[0][i] = csub(v[0][i], cscale(dot, 2.0 * kc));
+          }
         }
       }
-      __syncthreads();  // kf reads are done before the inverse transform's exchanges
+      __syncthreads();  // kf reads are done before the inverse transform's exchanges (or the next tile)
     }
     if (PEER && !parseval_only) {
       if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
@@ -194,7 +217,8 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
       }
       __syncthreads();  // the slot's exchange reads are done before the next tile lands
     } else if (!parseval_only) {
-      if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
+      // (the explicit barrier below orders the inverse's last exchange reads)
+      if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true, false>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
       __syncthreads();  // every exchange read is done before outputs overwrite the slot
       const bool inv_layout = (MODE != COL_FWD);
 #pragma unroll
@@ -205,9 +229,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, 1)
         col3_store(f == 0 ? &tmA : &tmB, slot, x0, col3_outer(g, o));
         bulk_commit();
       }
-    } else {
-      __syncthreads();  // the slot is consumed
-    }
+    }  // parseval-only tiles: the projection's closing barrier released the slot
   }
   if (threadIdx.x == 0) bulk_wait0();  // stores have landed in global memory
   if constexpr (PEER) __threadfence_system();  // peer stores visible before the host-level barrier

@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
     }
     PHASE_MARK(4);
     if (!parseval_only) {
-      fft_line<L, E, 1, true>(v, t, twy, SmemBuf{xbuf, 0}, hsync);
+      // (no tail barrier: the hsync below orders the last exchange reads)
+      fft_line<L, E, 1, true, false>(v, t, twy, SmemBuf{xbuf, 0}, hsync);
       PHASE_MARK(5);
       // outputs -> slot in the tensor layout, then one TMA store per line;
       // the barrier first: another warp of this half may still be reading its
@@ -206,9 +207,7 @@ __global__ void __launch_bounds__(ColTma<L>::THREADS, ColTma<L>::MINB)
         tma_store_4d(&tmA, slot, 2 * x, 0, 0, 0);
         bulk_commit();
       }
-    } else {
-      hsync();  // slot s consumed
-    }
+    }  // parseval-only lines: the forward transform's tail barrier was the slot's last use
     PHASE_MARK(6);
     if (ht == 0) mbar_arrive(&cbars[s]);  // after the hsync above: every thread of this half is done with slot s
     if (ht == 0 && k + K::NSLOT < nmine) {
