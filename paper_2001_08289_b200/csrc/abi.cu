@@ -123,10 +123,13 @@ int ensure_registry() {
   }
   for (int lg = 1; lg <= MAX_LG; ++lg) {
     LTable& t = r.tab[lg];
-    KInfo* all[4 + 4 + KC_COUNT + 2];  // NOLINT
+    KInfo* all[4 + 4 + 3 + KC_COUNT + 2];  // NOLINT
     int n = 0;
     all[n++] = &t.row_fwd;
     all[n++] = &t.row_inv;
+    all[n++] = &t.s1l[0];
+    all[n++] = &t.s1l[1];
+    all[n++] = &t.s3l;
     for (int s = 0; s < 4; ++s) all[n++] = &t.s1[s];
     for (int s = 0; s < 4; ++s) all[n++] = &t.s3[s];
     for (int c = 0; c < KC_COUNT; ++c) all[n++] = &t.col[c];
@@ -389,9 +392,9 @@ void fill_scalars(Args& a, const fftc_params* pr, int d, long long N) {
 }
 
 // ---- optional per-kernel timing (fftc_profile): event pairs per launch ----
-enum KindId { K_SWEEP1 = 0, K_MID, K_SWEEP3, K_YFWD, K_YINV, K_INIT, K_FINAL, K_OP, K_NKIND };
+enum KindId { K_SWEEP1 = 0, K_MID, K_SWEEP3, K_YFWD, K_YINV, K_INIT, K_FINAL, K_OP, K_PARSEVAL, K_NKIND };
 const char* kKindName[K_NKIND] = {"sweep1_rows_fwd", "sweep2_cols_gamma", "sweep3_rows_inv", "y_fwd_3d",
-                                  "y_inv_3d", "init", "finalize", "operator"};
+                                  "y_inv_3d", "init", "finalize", "operator", "z_parseval_3d"};
 struct KindStat {
   long long launches = 0;
   double ms = 0.0;
@@ -601,13 +604,75 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     use_graph = !general && !g_profile && pr->max_iters <= (1 << 20) && !getenv("FFTC_NO_GRAPH") && !debug_sync();
   }
   // graph mode runs the whole loop in one launch: the device keeps every record
-  const int hist_ring = use_graph ? (int)std::max<int64_t>(pr->max_iters, 16) : 1024;
+  const int hist_ring = use_graph ? (int)std::max<int64_t>(std::min<int64_t>(pr->max_iters, 1 << 20), 16) : 1024;
   const size_t partial_cap = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   char* ws = nullptr;
+  char* ws_lean = nullptr;  // per-row compact offsets of the memory-lean schedule
   const bool two_work = (scheme == FFTC_EM || scheme == FFTC_EM_SUB);  // B holds the flux transform
   const bool chi_perm = !general && nx >= 16;  // thread-blocked chi rows for the TMA row sweeps
-  const size_t ws_bytes = fld * (nslots + (two_work ? 2 : 1)) + sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring +
-                          sizeof(DevState) + sizeof(int2) * (size_t)ny * nz + (chi_perm ? (size_t)N + 256 : 0) + 8192;
+  const size_t small_bytes = sizeof(double) * partial_cap + sizeof(double) * 3 * hist_ring + sizeof(DevState) +
+                             sizeof(int2) * (size_t)ny * nz + 8192;
+  size_t ws_bytes = fld * (nslots + (two_work ? 2 : 1)) + small_bytes + (chi_perm ? (size_t)N + 256 : 0);
+  // Memory-lean em_sub schedule (3-D, TMA row and column passes): S/T slots
+  // compacted to the phase-1 voxels, and the flux transform Jq run on its own
+  // ahead of the residual field's, through ONE work field: per voxel
+  // 16d (Q) + 2*16d*f (S, T) + 16d (A) + 2 (rank codes) bytes instead of
+  // 5*16d + 1 -- at 1024^3 with f = 0.3, 137 GB instead of 259 GB (SURVEY 7,
+  // "memory at 1024^3").  Chosen when the normal workspace does not fit the
+  // free device memory; FFTC_LEAN=1/0 forces it on/off.  Results are bit
+  // identical to the normal schedule (same arithmetic, reordered launches).
+  const LTable& TXl = R.tab[lgx];
+  const bool lean_ok = scheme == FFTC_EM_SUB && d == 3 && !general && nx >= 512 && ny >= 256 && ny <= 1024 &&
+                       nz >= 256 && nz <= 1024 && TXl.s1l[0].max_active > 0 && TXl.s1l[1].max_active > 0 &&
+                       TXl.s3l.max_active > 0;
+  bool lean = false;
+  if (lean_ok) {
+    if (const char* lv = getenv("FFTC_LEAN")) {
+      lean = atoi(lv) != 0;
+    } else {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if (ws_bytes + ((size_t)1 << 30) > fr) {  // cached pool blocks count as used: release them, ask again
+        cudaMemPool_t pool;
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          cudaStreamSynchronize(s);
+          cudaMemPoolTrimTo(pool, 0);
+        }
+        cudaMemGetInfo(&fr, &tot);
+        lean = ws_bytes + ((size_t)1 << 30) > fr;
+      }
+    }
+  }
+  long long M = 0;
+  if (lean) {
+    // phase-1 voxels per row -> exclusive offsets (host scan of ny*nz counts)
+    const long long rows = ny * nz;
+    CK(cudaMallocAsync((void**)&ws_lean, sizeof(long long) * (size_t)(rows + 1), s));
+    {
+      unsigned g = (unsigned)std::min<long long>((rows + 7) / 8, (long long)R.num_sms * 8);
+      const uint8_t* chi = pb->chi;
+      long long* cnt = (long long*)ws_lean;
+      int nxi = (int)nx;
+      void* ca[] = {(void*)&chi, (void*)&nxi, (void*)&rows, (void*)&cnt};
+      CK(cudaLaunchKernel((const void*)k_row_counts, dim3(g), dim3(256), ca, 0, s));
+    }
+    std::vector<long long> off((size_t)rows + 1);
+    CK(cudaMemcpyAsync(off.data(), ws_lean, sizeof(long long) * (size_t)rows, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    long long acc = 0;
+    for (long long r = 0; r < rows; ++r) {
+      const long long c = off[(size_t)r];
+      off[(size_t)r] = acc;
+      acc += c;
+    }
+    off[(size_t)rows] = acc;
+    M = acc;
+    CK(cudaMemcpyAsync(ws_lean, off.data(), sizeof(long long) * (size_t)(rows + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // `off` leaves scope
+    ws_bytes = 2 * fld + 2 * sizeof(double2) * (size_t)d * (size_t)std::max<long long>(M, 1) + small_bytes +
+               2 * (size_t)N + 512;
+  }
   CK(cudaMallocAsync((void**)&ws, ws_bytes, s));
   size_t o = 0;
   auto carve = [&](size_t bytes) {
@@ -615,15 +680,26 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
     o += (bytes + 255) & ~(size_t)255;
     return p;
   };
-  for (int i = 0; i < nslots; ++i) a.X[i] = (double2*)carve(fld);
-  a.A = (double2*)carve(fld);
-  a.B = two_work ? (double2*)carve(fld) : a.A;
+  if (lean) {
+    const size_t cfld = sizeof(double2) * (size_t)d * (size_t)std::max<long long>(M, 1);
+    a.X[0] = (double2*)carve(fld);
+    a.X[1] = (double2*)carve(cfld);
+    a.X[2] = (double2*)carve(cfld);
+    a.A = a.B = (double2*)carve(fld);
+    a.rowoff = (const long long*)ws_lean;
+    a.M = M;
+    a.chiR = (const uint16_t*)carve(2 * (size_t)N);
+  } else {
+    for (int i = 0; i < nslots; ++i) a.X[i] = (double2*)carve(fld);
+    a.A = (double2*)carve(fld);
+    a.B = two_work ? (double2*)carve(fld) : a.A;
+  }
   a.partials = (double*)carve(sizeof(double) * partial_cap);
   a.history = (double*)carve(sizeof(double) * 3 * hist_ring);
   a.hist_cap = hist_ring;
   a.st = (DevState*)carve(sizeof(DevState));
   a.row_ext = (const int2*)carve(sizeof(int2) * (size_t)ny * nz);
-  a.chiT = chi_perm ? (const uint8_t*)carve((size_t)N) : nullptr;
+  a.chiT = (chi_perm && !lean) ? (const uint8_t*)carve((size_t)N) : nullptr;
   a.dbg = getenv("FFTC_PHASE") ? (unsigned long long*)carve(sizeof(unsigned long long) * 8) : nullptr;
   if (a.dbg) CK(cudaMemsetAsync(a.dbg, 0, sizeof(unsigned long long) * 8, s));
   a.outE = (double2*)E;
@@ -673,7 +749,10 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       unsigned g = (unsigned)std::min<long long>((rows + 7) / 8, (long long)R.num_sms * 8);
       void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
       if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) break;
-      if (chi_perm) {
+      if (lean) {  // rank codes of the compact S/T slots
+        void* ra[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiR};
+        if ((rc = Lc.raw((const void*)k_chi_rank16, g, 256, 0, ra, K_INIT))) break;
+      } else if (chi_perm) {
         const long long chunks = rows * (nx / 16);
         unsigned gp = (unsigned)std::min<long long>((chunks + 255) / 256, (long long)R.num_sms * 16);
         void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT};
@@ -725,11 +804,30 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       yf.nstrips = (int)(nx / 2);
     }
     // 3-D TMA column passes (cols3_tma.cuh) where the line lengths allow
-    Col3Pass zmid, yfwd, yinv;
+    Col3Pass zmid, yfwd, yinv, zpar;
     const PeerOut* no_peer = nullptr;
     a.zbs = 0;
     g_last_zbs = 0;
-    if (d == 3 && !general) {
+    if (lean) {
+      // one work field: y forward and the projection pass on A alone; the
+      // residual pass reads A through the "flux field" map (every tile
+      // Parseval-only, f0 = 1) and runs the monitor; the residual field's
+      // projection pass leaves the monitor alone
+      const int zbs = zblock_shift(nx, ny, nz);
+      const KInfo& kz = TZ.col[KC_MID3T_EM];
+      if (!(zbs > 0 && col3_pass_zblk(zpar, kz, a, a.A, a.A, 2, zbs, 1) &&
+            col3_pass_zblk(zmid, kz, a, a.A, nullptr, 2, zbs, 1) &&
+            col3_pass_zblk(yfwd, TY.col[KC_FWD3T], a, a.A, nullptr, 1, zbs, 1) &&
+            col3_pass_zblk(yinv, TY.col[KC_INV3T], a, a.A, nullptr, 1, zbs, 1))) {
+        g_err = "memory-lean em_sub schedule: the z-blocked TMA column passes are unavailable for this grid";
+        rc = 3;
+        break;
+      }
+      zpar.g.f0 = 1;
+      zmid.g.no_monitor = 1;
+      a.zbs = zbs;
+      g_last_zbs = zbs | 256;
+    } else if (d == 3 && !general) {
       // z-blocked work fields when all three column passes run on TMA tiles
       const int zbs = zblock_shift(nx, ny, nz);
       const KInfo& kz = TZ.col[em_type ? KC_MID3T_EM : KC_MID3T_BASIC];
@@ -788,9 +886,30 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       }
     };
 
+    // memory-lean em_sub iteration (solvers.py:395-432 in two halves): the
+    // flux Jq's forward transform and residual (Parseval) with the monitor,
+    // then -- unless stopped -- the residual field Rq's transform, (I - 2
+    // Gamma^), inverse and the state update, all through work field A
+    auto launch_lean = [&](Launcher& L) -> int {
+      int r;
+      void* ay[] = {&a, &yfwd.g, &yfwd.mA, &yfwd.mB, &no_peer};
+      void* azp[] = {&a, &zpar.g, &zpar.mA, &zpar.mB, &no_peer};
+      void* azm[] = {&a, &zmid.g, &zmid.mA, &zmid.mB, &no_peer};
+      void* ayi[] = {&a, &yinv.g, &yinv.mA, &yinv.mB, &no_peer};
+      if ((r = L.go(TX.s1l[0], row_lines, a1, K_SWEEP1))) return r;
+      if ((r = L.go(*yfwd.k, yfwd.tiles, ay, K_YFWD))) return r;
+      if ((r = L.go(*zpar.k, zpar.tiles, azp, K_PARSEVAL))) return r;
+      if ((r = L.go(TX.s1l[1], row_lines, a1, K_SWEEP1))) return r;
+      if ((r = L.go(*yfwd.k, yfwd.tiles, ay, K_YFWD))) return r;
+      if ((r = L.go(*zmid.k, zmid.tiles, azm, K_MID))) return r;
+      if ((r = L.go(*yinv.k, yinv.tiles, ayi, K_YINV))) return r;
+      return L.go(TX.s3l, row_lines, a1, K_SWEEP3);
+    };
+
     // one reference iteration (solvers.py:300-321 / :395-432) = these launches
     auto launch_iter = [&](Launcher& L) -> int {
       if (general) return launch_gen(L);
+      if (lean) return launch_lean(L);
       int r = L.go(TX.s1[scheme], row_lines, a1, K_SWEEP1);
       if (r) return r;
       if (d == 3) {
@@ -963,6 +1082,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   out->kernel_launches = Lc.count;
   g_launches += Lc.count;
   cudaFreeAsync(ws, s);
+  if (ws_lean) cudaFreeAsync(ws_lean, s);
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   if (!rc) {
@@ -1291,6 +1411,23 @@ int fftc_solve_batch(const fftc_problem* pb, const fftc_params* params, int32_t 
     std::lock_guard<std::mutex> lk(g_prof_mu);
     if (g_profile) width = 1;  // per-kernel statistics are collected in launch order
   }
+  if (width > 1 && pb) {
+    // every concurrent point holds its own workspace (state slots + work
+    // fields, fftc_solve): run only as many at once as the free device
+    // memory holds, down to one at a time for large grids (a 512^3 em_sub
+    // point alone needs ~32 GB)
+    const long long N = pb->n[0] * pb->n[1] * (pb->d == 3 ? pb->n[2] : 1);
+    size_t per = 0;
+    for (int32_t i = 0; i < n_points; ++i) {
+      const int sc = params[i].scheme;
+      const int nfld = (sc == FFTC_EM_SUB ? 3 : (sc == FFTC_BASIC_SUB ? 2 : 1)) +
+                       ((sc == FFTC_EM || sc == FFTC_EM_SUB) ? 2 : 1);
+      per = std::max(per, (size_t)nfld * sizeof(double2) * (size_t)pb->d * (size_t)N + (size_t)N + (32u << 20));
+    }
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && per > 0)
+      width = std::max(1, std::min<int>(width, (int)std::min<size_t>((size_t)(0.85 * (double)fr) / per, 64)));
+  }
   if (width <= 1) {
     for (int32_t i = 0; i < n_points; ++i) {
       int rc = fftc_solve(pb, &params[i], histories + (size_t)i * history_cap * 3, history_cap, nullptr, nullptr,
@@ -1402,7 +1539,8 @@ int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, 
   a.dist = 1;
   const int nslots = pr->scheme == FFTC_EM_SUB ? 3 : (pr->scheme == FFTC_BASIC_SUB ? 2 : 1);
   const size_t fld = sizeof(double2) * (size_t)d * N_l;
-  const int hist_cap = (int)std::max<int64_t>(pr->max_iters, 16);
+  // a ring: fftc_slab_monitor hands every record to the caller as it is written
+  const int hist_cap = 1024;
   const size_t pc = (size_t)R.num_sms * 64 * NQMAX + 16 * NQMAX;
   const size_t bytes = fld * nslots + sizeof(double) * pc + sizeof(double) * 3 * hist_cap + sizeof(DevState) +
                        sizeof(int2) * (size_t)ny * sd->nzl + sizeof(double) * 8 + (size_t)N_l + 256 + 8192;

@@ -95,8 +95,9 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
   const int nmine = (int)blockIdx.x < tiles ? (tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   auto coords = [&](int k, int& f, int& o, int& x0) {
     const int tile = (int)blockIdx.x + k * (int)gridDim.x;
-    f = tile / per_field;
-    const int r = tile - f * per_field;
+    const int fl = tile / per_field;
+    const int r = tile - fl * per_field;
+    f = g.f0 + fl;
     o = r / nstrips;
     x0 = (r - o * nstrips) * W;
   };
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
   if constexpr (PEER) __threadfence_system();  // peer stores visible before the host-level barrier
   if constexpr (MID) {
     double in[1] = {acc}, tot[1];
-    if (grid_reduce<1>(in, tot, a) && threadIdx.x == 0 && !a.op_mode) {
+    if (grid_reduce<1>(in, tot, a) && threadIdx.x == 0 && !a.op_mode && !g.no_monitor) {
       if (a.dist) a.st->parseval = tot[0] / a.inv_n;
       else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
     }

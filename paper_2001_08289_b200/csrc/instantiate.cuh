@@ -92,6 +92,9 @@ inline void fill_tma(LTable& t) {
     FFTC_TMA(BASIC_SUB)
     FFTC_TMA(EM_SUB)
 #undef FFTC_TMA
+    t.s1l[0] = make(k_rows_tma<EM_SUB, 1, LL, 1>, RowTma<EM_SUB, 1, LL, 1>::THREADS, RowTma<EM_SUB, 1, LL, 1>::SMEM, 1);
+    t.s1l[1] = make(k_rows_tma<EM_SUB, 1, LL, 2>, RowTma<EM_SUB, 1, LL, 2>::THREADS, RowTma<EM_SUB, 1, LL, 2>::SMEM, 1);
+    t.s3l = make(k_rows_tma<EM_SUB, 3, LL, 3>, RowTma<EM_SUB, 3, LL, 3>::THREADS, RowTma<EM_SUB, 3, LL, 3>::SMEM, 1);
   }
 }
 

@@ -31,6 +31,8 @@ struct LTable {
   int col3_w = 0;      // strip width of the 3-D mid kernels
   KInfo s1[4];         // sweep 1 per scheme
   KInfo s3[4];         // sweep 3 per scheme
+  KInfo s1l[2];        // memory-lean em_sub: sweep 1 of Jq alone, of Rq alone (compact S/T)
+  KInfo s3l;           // memory-lean em_sub: sweep 3 over compact S/T
   KInfo col[KC_COUNT];
   KInfo row_fwd, row_inv;  // plain row transforms (operator API)
 };

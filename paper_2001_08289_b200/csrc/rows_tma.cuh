@@ -24,11 +24,17 @@ namespace fftc {
 #ifndef FFTC_ROW_E
 #define FFTC_ROW_E 16
 #endif
-template <int S, int SW, int L>
+// Variant V of the em_sub row sweeps for the memory-lean schedule (abi.cu,
+// compact S/T slots, one work field): 0 = the normal sweeps; 1 = sweep 1 of
+// the flux channel Jq alone; 2 = sweep 1 of the residual field Rq alone;
+// 3 = sweep 3 over compact slots.  V > 0 stages rank codes (chiR, 2 bytes per
+// voxel) instead of phase flags.
+template <int S, int SW, int L, int V = 0>
 struct RowTma {
   static constexpr int E = FFTC_ROW_E;
   static constexpr int T = L / E;
-  static constexpr int CH = (SW == 1) ? Sweep1Traits<S>::C : 1;
+  static constexpr bool LEAN = V != 0;
+  static constexpr int CH = (SW == 1 && !LEAN) ? Sweep1Traits<S>::C : 1;
   static constexpr int THREADS = CH * T;
   static constexpr bool X0_ROW = (SW == 3) && (S == BASIC || S == BASIC_SUB);  // extra staged row
   // sweep 1 of the substituted schemes also stages its S (and T) rows over
@@ -38,7 +44,8 @@ struct RowTma {
   static constexpr int LP = Plan<L, E>::LP;
   static constexpr int ST_OFF = LP + (X0_ROW ? L : 0);
   static constexpr int CHI_OFF = ST_OFF + ST_ROWS * LP;     // double2 units
-  static constexpr int STAGE = CHI_OFF + L / 16;            // chi row = L bytes
+  static constexpr int CHI_BYTES = LEAN ? 2 * L : L;        // phase flags (or rank codes) of the row
+  static constexpr int STAGE = CHI_OFF + CHI_BYTES / 16;
   // twiddle table copied to shared memory (swizzled, L/2 entries) instead of
   // read through L1 (~39 KB left beside the stages), paid for with a
   // single-stage ring; measured at 2048^2 (us): sweep 1 em 116.5 -> 114.8,
@@ -62,7 +69,7 @@ struct RowTma {
   static constexpr int XBUF = (CH == 2 && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
   static constexpr int TWOFF = NSTAGE * STAGE + XBUF;              // double2 units
   static constexpr int SMEM = (TWOFF + (TWS ? L / 2 : 0)) * (int)sizeof(double2);
-  static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + L);
+  static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + CHI_BYTES);
   // resident CTAs per SM the register budget is sized for: the tuned values
   // for sweep 3 and at L != 1024; sweep-1 rows of 1024 (64 threads per
   // channel) fill the SM up to 16 warps or the shared-memory limit, whichever
@@ -74,10 +81,10 @@ struct RowTma {
   static constexpr int MINB = (L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1);
 };
 
-template <int S, int SW, int L>
+template <int S, int SW, int L, int V = 0>
 __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, uint64_t* bar, long long line,
                                                long long rows) {
-  using K = RowTma<S, SW, L>;
+  using K = RowTma<S, SW, L, V>;
   const int c = (int)(line / rows);
   const long long row = line - (long long)c * rows;
   const size_t off = (size_t)c * a.N + (size_t)row * L;
@@ -101,7 +108,10 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
       if constexpr (K::ST_ROWS > 1) bulk_g2s(stage + K::ST_OFF + K::LP + x0, a.X[2] + off + x0, nb, bar);
     }
   }
-  bulk_g2s(stage + K::CHI_OFF, a.chiT + (size_t)row * L, (unsigned)L, bar);  // thread-blocked chi row
+  if constexpr (K::LEAN)
+    bulk_g2s(stage + K::CHI_OFF, a.chiR + (size_t)row * L, (unsigned)K::CHI_BYTES, bar);  // rank codes
+  else
+    bulk_g2s(stage + K::CHI_OFF, a.chiT + (size_t)row * L, (unsigned)L, bar);  // thread-blocked chi row
 }
 
 // a thread's 16 phase flags (chiT row bytes t*16 .. t*16+15, element i = byte i)
@@ -114,25 +124,64 @@ __device__ __forceinline__ ChiBytes16 load_chi16(const uint8_t* chi_s, int t) {
   return ChiBytes16{{c.x, c.y, c.z, c.w}};
 }
 
-template <int S, int SW, int L>
+// a thread's 16 rank codes of the compact layout (chiR row entries t*16 ..
+// t*16+15): element i is phase 1 when its code is nonzero, and its S/T slot
+// is the row's compact base + code - 1
+struct ChiCodes16 {
+  uint32_t w[8];
+  __device__ __forceinline__ int code(int i) const { return (int)((w[i >> 1] >> ((i & 1) << 4)) & 0xffffu); }
+  __device__ __forceinline__ bool in1(int i) const { return code(i) != 0; }
+};
+__device__ __forceinline__ ChiCodes16 load_codes16(const uint8_t* chi_s, int t) {
+  const uint4 c0 = *reinterpret_cast<const uint4*>(chi_s + 32 * t);
+  const uint4 c1 = *reinterpret_cast<const uint4*>(chi_s + 32 * t + 16);
+  return ChiCodes16{{c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w}};
+}
+template <bool LEAN>
+struct PhaseRow;
+template <>
+struct PhaseRow<false> {
+  using type = ChiBytes16;
+  static __device__ __forceinline__ ChiBytes16 load(const uint8_t* chi_s, int t) { return load_chi16(chi_s, t); }
+};
+template <>
+struct PhaseRow<true> {
+  using type = ChiCodes16;
+  static __device__ __forceinline__ ChiCodes16 load(const uint8_t* chi_s, int t) { return load_codes16(chi_s, t); }
+};
+// S/T slot of element i of this thread: full-grid (off + x) or compact (base + code - 1)
+__device__ __forceinline__ size_t st_slot(const ChiBytes16&, int, size_t off, int x) { return off + x; }
+__device__ __forceinline__ size_t st_slot(const ChiCodes16& cc, int i, size_t base, int) {
+  return base + (size_t)(cc.code(i) - 1);
+}
+
+template <int S, int SW, int L, int V = 0>
 constexpr bool rows_prefetch_slots() {
-  return (S == BASIC_SUB || S == EM_SUB) && RowTma<S, SW, L>::ST_ROWS == 0;
+  return (S == BASIC_SUB || S == EM_SUB) && RowTma<S, SW, L, V>::ST_ROWS == 0;
 }
 
 // L2 prefetch of the phase-1 extent of the S/T (and em_sub sweep-3 Q) rows;
 // `ext` (that line's row_ext entry) was loaded one line earlier so the
 // prefetching warp never waits on it in front of the block barrier
-template <int S, int SW, int L>
+template <int S, int SW, int L, int V = 0>
 __device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, int line, int lines, int rows, int2 ext) {
-  if (!rows_prefetch_slots<S, SW, L>() || line >= lines) return;
+  if (!rows_prefetch_slots<S, SW, L, V>() || line >= lines) return;
   const int c = line / rows;
   const int row = line - c * rows;
   if (ext.x >= ext.y) return;
   const size_t off = (size_t)c * a.N + (size_t)row * L + (ext.x & ~1);
   const unsigned nb = (unsigned)((ext.y - (ext.x & ~1)) * sizeof(double2) + 15) & ~15u;
   if (SW == 3 && S == EM_SUB) l2_prefetch(a.X[0] + off, nb);
-  l2_prefetch(a.X[1] + off, nb);
-  if (S == EM_SUB) l2_prefetch(a.X[2] + off, nb);
+  if constexpr (V != 0) {  // compact slots: the row's phase-1 run is contiguous
+    const long long b = a.rowoff[row], e = a.rowoff[row + 1];
+    const size_t coff = (size_t)c * a.M + (size_t)b;
+    const unsigned cb = (unsigned)((e - b) * (long long)sizeof(double2));
+    l2_prefetch(a.X[1] + coff, cb);
+    l2_prefetch(a.X[2] + coff, cb);
+  } else {
+    l2_prefetch(a.X[1] + off, nb);
+    if (S == EM_SUB) l2_prefetch(a.X[2] + off, nb);
+  }
 }
 
 // em_sub sweep 1 with its two channels (Rq: channel 0, Jq: channel 1): thread
@@ -179,18 +228,20 @@ __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)
   }
 }
 
-template <int S, int SW, int L>
-__global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::MINB) k_rows_tma(Args a) {
-  using K = RowTma<S, SW, L>;
+template <int S, int SW, int L, int V = 0>
+__global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L, V>::MINB) k_rows_tma(Args a) {
+  using K = RowTma<S, SW, L, V>;
+  static_assert(V == 0 || S == EM_SUB, "the compact variants are em_sub sweeps");
+  static_assert(V == 0 || (SW == 1) == (V != 3), "variants 1, 2 are sweep 1; variant 3 is sweep 3");
   constexpr int E = K::E, T = K::T, CH = K::CH;
-  constexpr int NQ = (SW == 1) ? Sweep1Traits<S>::NQ : 6;
+  constexpr int NQ = (SW == 1) ? (V == 2 ? 1 : Sweep1Traits<S>::NQ) : 6;
   constexpr bool INV = (SW == 3);
   extern __shared__ __align__(128) double2 smem[];
   __shared__ uint64_t bars[K::NSTAGE];
   __shared__ double2 sdelta[3];
   if (a.st->stopped) return;
   const int t = threadIdx.x % T, ch = threadIdx.x / T;
-  const bool jchan = (ch == CH - 1);
+  const bool jchan = V == 1 ? true : (V == 2 ? false : (ch == CH - 1));
   // 32-bit line bookkeeping (axes <= 4096, so rows * d <= 3 * 2^24): keeps the
   // loop state in registers instead of local memory
   const int rows = a.ny * a.nz;
@@ -204,13 +255,13 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
   if constexpr (K::TWS)
     for (int i = threadIdx.x; i < L / 2; i += blockDim.x) smem[K::TWOFF + tw_swz(i)] = __ldg(&a.tw[0][i]);
   // phase-1 extent of the line after next, for the S/T prefetch
-  const bool pf = rows_prefetch_slots<S, SW, L>() && threadIdx.x == blockDim.x - 1;
+  const bool pf = rows_prefetch_slots<S, SW, L, V>() && threadIdx.x == blockDim.x - 1;
   int2 ext_next = make_int2(0, 0);
   if (pf && (int)blockIdx.x + (int)gridDim.x < lines) ext_next = a.row_ext[((int)blockIdx.x + (int)gridDim.x) % rows];
   __syncthreads();
   if (threadIdx.x == 0)
     for (int s = 0; s < K::NSTAGE && s < nmine; ++s)
-      rows_tma_issue<S, SW, L>(a, smem + s * K::STAGE, &bars[s], blockIdx.x + (long long)s * gridDim.x, rows);
+      rows_tma_issue<S, SW, L, V>(a, smem + s * K::STAGE, &bars[s], blockIdx.x + (long long)s * gridDim.x, rows);
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
@@ -231,10 +282,12 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
       const int2 ext = ext_next;
       const int l2 = line + 2 * (int)gridDim.x;
       if (l2 < lines) ext_next = a.row_ext[l2 % rows];
-      rows_tma_prefetch_slots<S, SW, L>(a, line + (int)gridDim.x, lines, rows, ext);
+      rows_tma_prefetch_slots<S, SW, L, V>(a, line + (int)gridDim.x, lines, rows, ext);
     }
     mbar_wait(&bars[s], parity);
-    const ChiBytes16 cb = load_chi16(chi_s, t);
+    const typename PhaseRow<K::LEAN>::type cb = PhaseRow<K::LEAN>::load(chi_s, t);
+    // S/T slot base of this line: the full-grid row, or the row's compact run
+    const size_t sbase = K::LEAN ? (size_t)c * a.M + (size_t)a.rowoff[row] : off;
     double2 v[1][E];
     constexpr bool SPLIT = (SW == 1 && S == EM_SUB && CH == 2 && K::ST_ROWS == 0);
     if constexpr (SPLIT) {
@@ -264,10 +317,10 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
           double2 sv = czero(), tv = czero();
           if (in1) {
             if constexpr (K::ST_ROWS >= 1) sv = st[K::ST_OFF + x];
-            else sv = a.X[1][off + x];
+            else sv = a.X[1][st_slot(cb, i, sbase, x)];
             if constexpr (S == EM_SUB) {
               if constexpr (K::ST_ROWS >= 2) tv = st[K::ST_OFF + K::LP + x];
-              else tv = a.X[2][off + x];
+              else tv = a.X[2][st_slot(cb, i, sbase, x)];
             }
           }
           const AugFlux f = apply_A(a, in1, q, sv, tv);
@@ -339,8 +392,8 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
           } else if constexpr (S == EM_SUB) {
             if (in1v[u]) {
               qv[u] = a.X[0][off + x];
-              sv[u] = a.X[1][off + x];
-              tv[u] = a.X[2][off + x];
+              sv[u] = a.X[1][st_slot(cb, b0 + u, sbase, x)];
+              tv[u] = a.X[2][st_slot(cb, b0 + u, sbase, x)];
             }
           }
         }
@@ -379,8 +432,8 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
             em_sub_update(a, in1, wq, ws, wt, qn, sn, tn);
             a.X[0][off + x] = qn;
             if (in1) {
-              a.X[1][off + x] = sn;
-              a.X[2][off + x] = tn;
+              a.X[1][st_slot(cb, b0 + u, sbase, x)] = sn;
+              a.X[2][st_slot(cb, b0 + u, sbase, x)] = tn;
             }
           }
           acc_c<NQ>(acc, c, qn);
@@ -390,15 +443,17 @@ __global__ void __launch_bounds__(RowTma<S, SW, L>::THREADS, RowTma<S, SW, L>::M
     __syncthreads();  // stage s fully consumed (exchange, chi, X0 row)
     if (threadIdx.x == 0 && k + K::NSTAGE < nmine) {
       fence_proxy_async();
-      rows_tma_issue<S, SW, L>(a, st, &bars[s], (long long)line + (long long)K::NSTAGE * gridDim.x, rows);
+      rows_tma_issue<S, SW, L, V>(a, st, &bars[s], (long long)line + (long long)K::NSTAGE * gridDim.x, rows);
     }
   }
   double tot[NQ];
   if (grid_reduce<NQ>(acc, tot, a) && threadIdx.x == 0) {
     if constexpr (SW == 1) {
-      for (int cc = 0; cc < a.d; ++cc)
-        a.st->jmean[cc] = make_double2(tot[2 * cc] * a.inv_n, tot[2 * cc + 1] * a.inv_n);
-      a.st->js2 = (NQ > 6) ? tot[NQ - 1] : 0.0;
+      if constexpr (V != 2) {  // (the residual-field sweep of the lean schedule carries no flux sums)
+        for (int cc = 0; cc < a.d; ++cc)
+          a.st->jmean[cc] = make_double2(tot[2 * cc] * a.inv_n, tot[2 * cc + 1] * a.inv_n);
+        a.st->js2 = (NQ > 6) ? tot[NQ - 1] : 0.0;
+      }
     } else {
       for (int cc = 0; cc < a.d; ++cc)
         a.st->delta[cc] = csub(a.e0[cc], make_double2(tot[2 * cc] * a.inv_n, tot[2 * cc + 1] * a.inv_n));

@@ -69,6 +69,14 @@ struct Args {
   // byte t*16 + i holds chi[t + i*nx/16], so a thread's 16 phase flags are one
   // 16-byte shared-memory load (k_chi_perm16)
   const uint8_t* chiT;
+  // Compact S/T slots (the memory-lean em_sub schedule, abi.cu): when rowoff
+  // is set, X[1] and X[2] hold only the phase-1 voxels -- row r's, in x
+  // order, at [rowoff[r], rowoff[r+1]) of each component's block of M --
+  // and chiR holds, in chiT's thread-blocked order, 0 for phase 2 and
+  // 1 + the voxel's rank among its row's phase-1 voxels.
+  const long long* rowoff;  // rows + 1 entries, or null (full-grid slots)
+  long long M;              // phase-1 voxel count (component stride of the compact slots)
+  const uint16_t* chiR;
   double2* X[3];  // state slots: e_raw | Q_raw, S_raw, T_raw
   double2* A;     // work field 0 (d*N)
   double2* B;     // work field 1 (d*N)
@@ -103,6 +111,22 @@ struct Args {
   double2 sinv;                    // 1/(1+s0)
   double2 cinv_p1, cinv_p2, cinv_p3;  // ((t-1)/(t+s0)) p_i
 };
+
+// index of voxel (row, x) in the thread-blocked row order of chiT / chiR
+// (16 elements per thread: x = t + i*nx/16 sits at 16 t + i)
+__device__ __forceinline__ long long tblock_index(long long row, int x, int nx) {
+  const int T = nx >> 4;
+  return row * nx + 16 * (x % T) + x / T;
+}
+
+// compact S/T slot of voxel p = row*nx + x, component c (lean layout), or -1
+// on phase 2
+__device__ __forceinline__ long long compact_slot(const Args& a, int c, long long p) {
+  const long long row = p / a.nx;
+  const int x = (int)(p - row * a.nx);
+  const int code = a.chiR[tblock_index(row, x, a.nx)];
+  return code ? (long long)c * a.M + a.rowoff[row] + (code - 1) : -1;
+}
 
 // element offset of row `row` = z*ny + y of component c of a work field (A/B)
 __device__ __forceinline__ size_t work_off(const Args& a, int c, long long row) {
@@ -623,7 +647,8 @@ struct Line3 {
   // tensor-map coordinates of outer line o: {.., (o >> obs) * om, o & (2^obs - 1), ..}
   // when om > 0 (y passes over the z-blocked layout), else {.., 0, o, ..}
   int obs, om;
-  int pad;
+  int f0;          // field of the first tile (1: a Parseval-only pass over field B's map)
+  int no_monitor;  // projection pass whose residual belongs to another launch
 };
 
 // Destinations of a column pass whose outputs go straight to the rank that
@@ -804,6 +829,50 @@ static __global__ void __launch_bounds__(256) k_chi_perm16(const uint8_t* __rest
   }
 }
 
+// phase-1 voxels per row (compact S/T layout): one warp per row
+static __global__ void __launch_bounds__(256) k_row_counts(const uint8_t* __restrict__ chi, int nx, long long rows,
+                                                         long long* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = warp; r < rows; r += nw) {
+    int n = 0;
+    for (int x = lane; x < nx; x += 32) n += chi[(size_t)r * nx + x] != 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) cnt[r] = n;
+  }
+}
+
+// rank codes of the compact layout (Args::chiR): one warp per row, lane l
+// scans x in [l*nx/32, (l+1)*nx/32) in order after a warp prefix sum of the
+// lanes' counts; codes land in the thread-blocked order of chiT
+static __global__ void __launch_bounds__(256) k_chi_rank16(const uint8_t* __restrict__ chi, int nx, long long rows,
+                                                         uint16_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int span = nx >= 32 ? nx / 32 : 1;
+  for (long long r = warp; r < rows; r += nw) {
+    const uint8_t* row = chi + (size_t)r * nx;
+    const int x0 = lane * span, x1 = min(nx, x0 + span);
+    int n = 0;
+    for (int x = x0; x < x1; ++x) n += row[x] != 0;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int rank = incl - n;
+    for (int x = x0; x < x1; ++x) {
+      const bool in1 = row[x] != 0;
+      out[tblock_index(r, x, nx)] = in1 ? (uint16_t)(rank + 1) : (uint16_t)0;
+      rank += in1;
+    }
+  }
+}
+
 // ============================================================================
 // 2-D projection sweep, component-split variant (the hot 2-D sweep 2).
 // One thread carries ONE component of one column (E = 16 per thread, radix-16
@@ -903,8 +972,16 @@ __global__ void __launch_bounds__(256) k_init(Args a) {
       double2 ws = f.js, wt = f.jt;
       double2 sn, tn;
       em_sub_update(a, in1, wq, ws, wt, q, sn, tn);
-      a.X[1][i] = sn;
-      a.X[2][i] = tn;
+      if (a.rowoff) {  // compact slots: phase-1 voxels only
+        if (in1) {
+          const long long ci = compact_slot(a, c, p);
+          a.X[1][ci] = sn;
+          a.X[2][ci] = tn;
+        }
+      } else {
+        a.X[1][i] = sn;
+        a.X[2][i] = tn;
+      }
     }
     a.X[0][i] = q;
     acc_c<NQ>(acc, c, q);
@@ -945,8 +1022,9 @@ __global__ void __launch_bounds__(256) k_finalize(Args a) {
       J = cmul(sigma_at(a, in1), E);
     } else {
       double2 q = a.X[0][i];
-      double2 s = in1 ? a.X[1][i] : czero();
-      double2 tt = (S == EM_SUB && in1) ? a.X[2][i] : czero();
+      const long long si = (a.rowoff && in1) ? compact_slot(a, c, p) : i;
+      double2 s = in1 ? a.X[1][si] : czero();
+      double2 tt = (S == EM_SUB && in1) ? a.X[2][si] : czero();
       AugFlux f = apply_A(a, in1, q, s, tt);
       double2 js;
       pinned_flux(a, in1, f.jq, f.js, dl, J, js);

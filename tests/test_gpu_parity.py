@@ -56,6 +56,10 @@ def _chi(geom):
     if kind == "random3d":
         rng = np.random.default_rng(geom["seed"])
         return rng.random((geom["n"],) * 3) < geom["frac"]
+    if kind == "c4medium":  # BASELINE config 4 recipe (frozen SHA-256 at 1024^3)
+        from paper_2001_08289_b200 import cell
+
+        return np.asarray(cell.c4_phase_map(geom["n"]).chi)
     raise ValueError(kind)
 
 
