@@ -6,6 +6,7 @@ fixed-point loops running as fused sm_100a CUDA sweeps behind a C ABI
 (``include/fftcond_b200.h``).  d = 2 (reference) and d = 3 (extension).
 """
 
+from .analysis import MisestimationReport, MisestimationRun, misestimation_report, misestimation_reports
 from .cell import (
     PhaseMap,
     build_cube_array,
@@ -82,6 +83,7 @@ __all__ = [
     "ConvergenceHistory", "DegenerateParamError", "HistoryRecord", "IntervalError", "PhaseMap",
     "PoleError", "RasterParseError", "SchemeKind", "SolveResult", "SolverConfig", "SpectralInterval",
     "SubstitutionParams", "SupportError", "TerminationStatus", "VectorField", "build_cube_array",
+    "MisestimationReport", "MisestimationRun", "misestimation_report", "misestimation_reports",
     "build_disk_array", "build_random_medium", "build_square_array", "build_uniform", "estimate_rate",
     "map_t", "map_z", "solve", "solve_basic", "solve_basic_sub", "solve_em", "solve_em_sub", "solve_p",
     "volume_fraction", "aux_constants", "inverse_map_t", "verify_sigma1", "apply_chi_aug", "apply_local_A",

@@ -20,7 +20,7 @@ import numpy as np
 class PhaseMap:
     """Immutable two-phase indicator; every axis even and >= 2."""
 
-    __slots__ = ("_chi", "_dev")
+    __slots__ = ("_chi", "__weakref__")
 
     def __init__(self, chi):
         arr = np.array(chi, dtype=bool)
@@ -30,7 +30,6 @@ class PhaseMap:
             raise ValueError(f"grid dims must be even and >= 2, got {arr.shape}")
         arr.flags.writeable = False
         self._chi = arr
-        self._dev = None  # device copy, created on first solve
 
     @property
     def chi(self) -> np.ndarray:

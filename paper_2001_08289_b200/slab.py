@@ -302,8 +302,11 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
             ok = ptrs is not None and be.set_peers(world, [p[0] for p in ptrs], [p[1] for p in ptrs],
                                                     [p[2] for p in ptrs])
             use_fused = _all_true(ok, dist, group, device, comm)
-            if ok and not use_fused:
-                raise BackendError("ranks disagree on fused transposes")  # cannot undo set_peers on this rank
+            some_fused = not _all_true(not ok, dist, group, device, comm)
+            if some_fused and not use_fused:
+                # set_peers cannot be undone on the ranks where it succeeded: every
+                # rank raises (the decision is collective), none waits in a collective
+                raise BackendError("ranks disagree on fused transposes")
         be.set_delta(global_delta(be.phase(PH_INIT)))
         history, rec = [], None
         for k in range(1, cfg.max_iters + 1):
@@ -325,6 +328,8 @@ def solve_slab(chi_global: np.ndarray, cfg: SolverConfig, *, group=None, backend
                 break
             be.set_delta(global_delta(be.phase(PH_ROWS_INV)))
         means = _allreduce(be.finalize(), dist, group, device)
+        if use_fused:
+            _barrier(dist, group, comm)  # no peer still stores into this rank's buffers when they are freed
         sstar = history[-1][0] if history else complex(rec[4], rec[5])
         return dict(status=_STATUS[int(rec[1])], degenerate_flux=bool(rec[2]), iterations=len(history),
                     sigma_star=sstar, history=history, fused=use_fused,

@@ -20,6 +20,8 @@ from __future__ import annotations
 import cmath
 import ctypes as C
 import math
+import threading
+import weakref
 from dataclasses import dataclass
 from enum import Enum
 
@@ -202,14 +204,33 @@ def _torch():
     return torch
 
 
+# Device copies of phase maps, per map (by identity: PhaseMap hashes its
+# whole indicator) and per device, dropped when the map is collected.
+_CHI_CACHE: dict = {}  # id(pmap) -> (weakref to pmap, {device index: tensor})
+_CHI_LOCK = threading.Lock()
+
+
 def _device_chi(pmap: PhaseMap, torch):
     dev = torch.cuda.current_device()
-    cached = pmap._dev
-    if cached is not None and cached.device.index == dev:
-        return cached
+    key = id(pmap)
+    with _CHI_LOCK:
+        ent = _CHI_CACHE.get(key)
+        if ent is not None and ent[0]() is pmap and dev in ent[1]:
+            return ent[1][dev]
     t = torch.from_numpy(pmap.chi.astype(np.uint8)).to(device="cuda")
-    pmap._dev = t
+    with _CHI_LOCK:
+        ent = _CHI_CACHE.get(key)
+        if ent is None or ent[0]() is not pmap:
+            ent = (weakref.ref(pmap, lambda _r, k=key: _CHI_CACHE.pop(k, None)), {})
+            _CHI_CACHE[key] = ent
+        ent[1][dev] = t
     return t
+
+
+def release_device_copies(pmap: PhaseMap) -> None:
+    """Drop the cached device copies of a phase map (1 GiB at 1024^3)."""
+    with _CHI_LOCK:
+        _CHI_CACHE.pop(id(pmap), None)
 
 
 def _check_grid(pmap: PhaseMap):

@@ -50,3 +50,26 @@ def test_sweep_1024_goldens():
         pytest.skip("no 1024^2 config-5 goldens")
     vals = list(g.values())
     _check(_run(vals, 1024), vals)
+
+
+def test_misestimation_reports_batched_match_sequential():
+    """analysis.py:166-201 batched: every run equals the same em_sub solve
+    made on its own (one fftc_solve_batch for all pairs)."""
+    import paper_2001_08289_b200 as fb
+
+    pm = fb.build_square_array(64, 0.5)
+    cfg = fb.SolverConfig(scheme=fb.SchemeKind.EYRE_MILTON_SUB, sigma1=1.0, tol=1e-8, max_iters=400,
+                          interval=fb.SpectralInterval(0.25, 4.0))
+    true_iv, bench_iv = fb.SpectralInterval(0.25, 4.0), fb.SpectralInterval(0.1, 10.0)
+    cases = [(2.0, true_iv, bench_iv), (10.0 + 1.0j, true_iv, bench_iv), (0.5, bench_iv, true_iv)]
+    reps = fb.misestimation_reports(pm, cases, cfg, rate_window=3)
+    assert len(reps) == 3
+    for (s1, tiv, aiv), rep in zip(cases, reps):
+        for iv, run in ((tiv, rep.true_run), (aiv, rep.assumed_run)):
+            one = fb.solve(pm, fb.SolverConfig(scheme=fb.SchemeKind.EYRE_MILTON_SUB, sigma1=s1, tol=1e-8,
+                                               max_iters=400, interval=iv))
+            assert (run.status, run.iterations, run.sigma_star) == (one.status, one.iterations, one.sigma_star)
+            assert run.interval is iv and run.wall_time > 0
+        assert rep.rate_penalty is None or abs(rep.rate_penalty) < 1
+    single = fb.misestimation_report(pm, 2.0, true_iv, bench_iv, cfg, rate_window=3)
+    assert single.true_run.sigma_star == reps[0].true_run.sigma_star
