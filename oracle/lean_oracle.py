@@ -64,12 +64,15 @@ def _slabs(n: int, parts: int):
 
 
 def par(n0: int, fn) -> list:
-    """fn(slice) over slabs of the outermost axis (length n0), in order."""
+    """fn(slice) over slabs of the outermost axis (length n0), in order, on
+    the thread pool.  Slabs are small (16 per thread, at least one plane) so
+    the temporaries of the pointwise expressions stay a small multiple of
+    threads x slab instead of a multiple of the grid."""
     nt = nthreads()
-    sls = _slabs(n0, nt)
-    if len(sls) == 1:
-        return [fn(sls[0])]
-    return list(_pool(len(sls)).map(fn, sls))
+    sls = _slabs(n0, 16 * nt)
+    if nt == 1 or len(sls) == 1:
+        return [fn(sl) for sl in sls]
+    return list(_pool(nt).map(fn, sls))
 
 
 def _cut(arr: np.ndarray, sl: slice) -> np.ndarray:
