@@ -67,3 +67,35 @@ def test_bad_arguments_are_errors_not_crashes():
     p.n[0], p.n[1], p.n[2] = 7, 8, 1  # odd axis: the reference's PhaseMap rejects it too
     rc = L.fftc_solve(C.byref(p), C.byref(par), None, 0, None, None, None, C.byref(res), None)
     assert rc == 3
+
+
+def test_reference_seam_binding_structs_and_host_errors():
+    """tests/ref_seam.py (the INTEGRATION.md binding): its ctypes structs match
+    the library's, and the reference's own validation still raises before any
+    device call once the seam is installed (solvers.py:221-240)."""
+    import pytest
+
+    import ref_seam
+    from paper_2001_08289_b200 import native
+
+    for a, b in ((ref_seam._Problem, native.Problem), (ref_seam._Params, native.Params),
+                 (ref_seam._Result, native.Result)):
+        assert C.sizeof(a) == C.sizeof(b) and [f[0] for f in a._fields_] == [f[0] for f in b._fields_]
+    assert hasattr(ref_seam.lib(), "fftc_solve_host")
+    try:
+        from paper_2001_08289_b200 import selftest
+
+        selftest.reference_module()
+        import fftcond
+    except Exception:
+        pytest.skip("reference package not installed (baseline/_ref)")
+    fc = fftcond
+    orig = fc.solvers._solve_h, fc.solvers._solve_aug
+    try:
+        ref_seam.install(fc)
+        assert fc.solvers._solve_h is not orig[0]
+        cfg = fc.SolverConfig(scheme=fc.SchemeKind.EYRE_MILTON, sigma1=-2.0)
+        with pytest.raises(fc.BranchCutError):
+            fc.solve(fc.build_square_array(8, 0.5), cfg)
+    finally:
+        fc.solvers._solve_h, fc.solvers._solve_aug = orig
