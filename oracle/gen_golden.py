@@ -26,8 +26,13 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-GOLDEN = os.path.join(REPO, "tests", "golden")
-REF_SRC = "/root/reference/pkg/src"
+# FFTC_GOLDEN_DIR: write fixtures elsewhere (the GPU box host writes under
+# gpurun_out/); FFTC_REF_SRC: where the live reference is importable from --
+# the read-only tree here, or its unmodified install under baseline/_ref on
+# the GPU box host (pip install --target)
+GOLDEN = os.environ.get("FFTC_GOLDEN_DIR") or os.path.join(REPO, "tests", "golden")
+REF_SRC = os.environ.get("FFTC_REF_SRC") or (
+    "/root/reference/pkg/src" if os.path.isdir("/root/reference/pkg/src") else os.path.join(REPO, "baseline", "_ref"))
 
 ALPHA, BETA = 0.25, 4.0  # configs/compare.cfg:14-15 (the reference's only interval)
 SEED = 20260809  # selftest.py:38
@@ -124,7 +129,7 @@ def run_case(case):
         out = dict(status=r.status.value, degenerate_flux=bool(r.degenerate_flux),
                    iterations=r.iterations, sigma_star=cplx(r.sigma_star), history=hist,
                    mean_E=[cplx(v) for v in _mean_vec(E)], mean_J=[cplx(v) for v in _mean_vec(J)],
-                   source="reference fftcond (live, /root/reference/pkg/src)")
+                   source=f"reference fftcond (live, {REF_SRC})")
         aug = r.aug_field
         fields = dict(E=E, J=J)
         if aug is not None:
