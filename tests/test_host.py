@@ -168,3 +168,48 @@ def test_no_cpu_fallback_without_gpu(monkeypatch):
         pytest.skip("GPU present")
     with pytest.raises(fb.BackendError):
         fb.solve(fb.build_square_array(8, 0.5), cfg_for(fb.SchemeKind.BASIC, 2.0))
+
+
+def test_bench_gpus_flag_relaunches_under_torchrun(monkeypatch):
+    """bench.py --gpus N without a torchrun environment relaunches itself as N
+    ranks (torch.distributed.run, 127.0.0.1); a WORLD_SIZE that disagrees with
+    --gpus is an error, not a silent single-GPU run."""
+    import subprocess
+    import types
+
+    import bench
+
+    seen = {}
+
+    def fake_run(cmd, *a, **k):
+        seen["cmd"] = cmd
+        return types.SimpleNamespace(returncode=0)
+
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(subprocess, "run", fake_run)
+    monkeypatch.setattr(bench.sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2"])
+    assert bench._relaunch(types.SimpleNamespace(gpus=4)) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"] and "--nproc-per-node=4" in cmd
+    assert "127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+    assert bench._relaunch(types.SimpleNamespace(gpus=1)) is None
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert bench._relaunch(types.SimpleNamespace(gpus=2)) is None
+    assert bench._relaunch(types.SimpleNamespace(gpus=4)) == 2
+
+
+def test_bench_byte_models():
+    """Per-launch algorithmic bytes add up to the
+    schedule totals quoted there."""
+    import bench
+
+    f = 0.25
+    V = 48.0
+    k = bench._bytes_per_voxel("em_sub", 3, f)
+    assert abs(sum(k.values()) - (14 * V + 7 * f * V + 2)) < 1e-9
+    assert abs(bench._survey_bytes("em_sub", 3, f) - (15 * V + 6 * f * V + 2)) < 1e-9
+    lean = bench._bytes_lean(f)
+    tot = sum(v * bench.LEAN_LAUNCHES.get(n, 1) for n, v in lean.items())
+    assert abs(tot - (15 * V + 9 * f * V + 6)) < 1e-9
+    k2 = bench._bytes_per_voxel("basic", 2, f)
+    assert abs(sum(k2.values()) - (7 * 32 + 2)) < 1e-9
