@@ -177,7 +177,14 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
           const double kc = comp == 0 ? kx : (comp == 1 ? ko : kl);
           const double k2 = kx * kx + ko * ko + kl * kl;
           const double ik2 = (k2 != 0.0) ? inv_k2(k2) * a.gscale : 0.0;
-          double2 dot = cadd(cadd(slot[pos * W + w], slot[(L + pos) * W + w]), slot[(2 * L + pos) * W + w]);
+          // k.F^ = (kx Fx + ky Fy) + kz Fz in the same order on every component
+          // thread; a thread's own term comes from its registers (comp is warp
+          // uniform), the other two from the slot
+          const double2 mine = cscale(v[0][i], kc);
+          const double2 s0 = comp == 0 ? mine : slot[pos * W + w];
+          const double2 s1 = comp == 1 ? mine : slot[(L + pos) * W + w];
+          const double2 s2 = comp == 2 ? mine : slot[(2 * L + pos) * W + w];
+          double2 dot = cadd(cadd(s0, s1), s2);
           dot = cscale(dot, ik2);
           if (MODE == MID_BASIC) {
             const double2 gc = cscale(dot, kc);
