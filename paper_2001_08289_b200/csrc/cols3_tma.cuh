@@ -72,6 +72,14 @@ __device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2*
                : "memory");
 }
 
+#ifndef FFTC_PEER_BULK
+#define FFTC_PEER_BULK 1
+#endif
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
 // PEER: outputs are written straight to their owning rank (PeerOut po,
 // device memory) instead of back through the slot and a TMA store -- the
 // decomposed solve's transposes fused into the pass that produces the data.
@@ -126,6 +134,9 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
     double2 v[1][E];
 #pragma unroll
     for (int i = 0; i < E; ++i) v[0][i] = slot[(comp * L + pos_first<L, E>(INV_ONLY, t, i)) * W + w];
+    // (peer bulk copies: each thread's copies out of the other slot have been
+    // read before thread 0 reloads it below)
+    if constexpr (PEER && FFTC_PEER_BULK) bulk_wait_read0();
     __syncthreads();  // every input is in registers: the slot becomes exchange scratch
     if (threadIdx.x == 0 && k + K::NSLOT - 1 < nmine) {
       // tile k+NSLOT-1 into the slot of tile k-1, whose store was committed one tile ago
@@ -198,6 +209,38 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
       __syncthreads();  // kf reads are done before the inverse transform's exchanges (or the next tile)
     }
     if (PEER && !parseval_only) {
+#if FFTC_PEER_BULK
+      // Outputs staged dense in the slot ([c][pos][w], as for the TMA store),
+      // then one bulk copy per (component, line position): the tile's W
+      // adjacent x-values are one contiguous 16W-byte run in the owning
+      // rank's slab, so the transpose leaves as bulk-copy requests of whole
+      // tile rows instead of 16-byte stores (NVLink to peers).
+      if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true, false>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
+      __syncthreads();  // every exchange read is done before outputs overwrite the slot
+      const bool inv_layout = (MODE != COL_FWD);
+#pragma unroll
+      for (int i = 0; i < E; ++i) slot[(comp * L + pos_last<L, E>(inv_layout, t, i)) * W + w] = v[0][i];
+      fence_proxy_async();
+      __syncthreads();
+      const int rq = po->rows_per_rank;
+      for (int r = threadIdx.x; r < 3 * L; r += (int)blockDim.x) {
+        const int cc = r / L, pos = r - cc * L;
+        const int q = pos / rq;
+        const long long p = pos - q * rq;
+        long long off;
+        if (po->zs > 0) {  // z-blocked destination slabs
+          const int zs = po->zs;
+          const long long O = po->outer0 + o;
+          const long long b = po->blk_line ? p : O, u = po->blk_line ? O : p;
+          const long long row = (((b >> zs) * po->bn + u) << zs) | (b & ((1 << zs) - 1));
+          off = cc * po->comp_stride + x0 + row * po->row_len;
+        } else {
+          off = cc * po->comp_stride + (po->outer0 + o) * po->outer_stride + x0 + p * po->line_stride;
+        }
+        bulk_s2g(po->dst[f][q] + off, slot + (cc * L + pos) * W, (unsigned)(W * sizeof(double2)));
+      }
+      bulk_commit();
+#else
       if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
       const bool inv_layout = (MODE != COL_FWD);
       const int rq = po->rows_per_rank;
@@ -224,6 +267,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
         }
       }
       __syncthreads();  // the slot's exchange reads are done before the next tile lands
+#endif
     } else if (!parseval_only) {
       // (the explicit barrier below orders the inverse's last exchange reads)
       if constexpr (MODE != COL_FWD) fft_line<L, E, 1, true, false>(v, t, tw, SmemBuf{xb, 0}, SyncAll{});
@@ -239,7 +283,7 @@ __global__ void __launch_bounds__(Col3Tma<L>::THREADS, Col3Tma<L>::MINB)
       }
     }  // parseval-only tiles: the projection's closing barrier released the slot
   }
-  if (threadIdx.x == 0) bulk_wait0();  // stores have landed in global memory
+  if (threadIdx.x == 0 || (PEER && FFTC_PEER_BULK)) bulk_wait0();  // stores have landed in global memory
   if constexpr (PEER) __threadfence_system();  // peer stores visible before the host-level barrier
   if constexpr (MID) {
     double in[1] = {acc}, tot[1];
