@@ -9,8 +9,10 @@ against the oracle restatement of the reference loops (solvers.py:280-331,
 * the first iterations AT the stated sizes (c3first: 512^3; c4first:
   1024^3 on the frozen medium), every history record within the protocol;
 * the memory-lean em_sub schedule (compact S/T, one work field -- what runs
-  C4's accelerated arm on one GPU) bit for bit against the normal schedule,
-  and against the 512^3 fixture.
+  C4's accelerated arm on one GPU) against the normal schedule to summation
+  order (the flux sums of a line are accumulated by one thread instead of
+  two, so records agree to ~1e-15 relative, not bit for bit), and against
+  the 512^3 fixture.
 Protocol: tests/parity.py."""
 
 from __future__ import annotations
@@ -38,12 +40,39 @@ def _sumsq_check(r, g, rel=1e-9):
     got = {"E": r.E_field, "J": r.J_field}
     if r.aug_field is not None:
         got.update(S=r.aug_field.S, T=r.aug_field.T)
+    e_scale = max(max(want["E"]), 1e-300) if "E" in want else 1.0
     for key, ref in want.items():
         data = got[key].data
         scale = max(max(ref), 1e-300)
+        # An auxiliary field that vanishes at the fixed point (T of a converged
+        # em_sub run: sum |T|^2 ~ 1e-10 against ~1e6 for E) is a residual-level
+        # quantity: its square follows the stopping residual, which the
+        # protocol (tests/parity.py) pins to 1e-4 relative, not 1e-10.
+        tol = 2e-4 if scale < 1e-12 * e_scale else rel
         for c, v in enumerate(ref):
             s = float(np.sum(np.abs(data[c]) ** 2))
-            assert abs(s - v) <= rel * scale, f"{g['case']['name']} {key}[{c}]: {s!r} vs {v!r}"
+            assert abs(s - v) <= tol * scale, f"{g['case']['name']} {key}[{c}]: {s!r} vs {v!r}"
+
+
+def _same_to_roundoff(a, b, fields=False):
+    """Two schedules of the same arithmetic (normal / memory-lean): equal
+    status and iteration count, every record equal to summation order."""
+    assert (a.status, a.iterations, a.degenerate_flux) == (b.status, b.iterations, b.degenerate_flux)
+    ha = np.array([[h.sigma_star.real, h.sigma_star.imag, h.residual] for h in a.history])
+    hb = np.array([[h.sigma_star.real, h.sigma_star.imag, h.residual] for h in b.history])
+    sa, sb = ha[:, 0] + 1j * ha[:, 1], hb[:, 0] + 1j * hb[:, 1]
+    assert np.max(np.abs(sa - sb) / np.abs(sa)) <= 1e-13
+    # the residual amplifies roundoff as it falls: eps * contrast / residual
+    assert np.max(np.abs(ha[:, 2] - hb[:, 2]) / (ha[:, 2] + 1e-10)) <= 1e-6
+    assert abs(a.sigma_star - b.sigma_star) <= 1e-13 * abs(a.sigma_star)
+    if fields:
+        assert np.allclose(a.mean_E, b.mean_E, rtol=0, atol=1e-13 * np.max(np.abs(a.mean_E)))
+        assert np.allclose(a.mean_J, b.mean_J, rtol=0, atol=1e-13 * np.max(np.abs(a.mean_J)))
+        for fa, fb_ in ((a.E_field, b.E_field), (a.J_field, b.J_field), (a.aug_field.S, b.aug_field.S),
+                        (a.aug_field.T, b.aug_field.T)):
+            da, db = fa.data, fb_.data
+            scale = max(float(np.max(np.abs(a.E_field.data))), float(np.max(np.abs(da))))
+            assert float(np.max(np.abs(da - db))) <= 1e-11 * scale
 
 
 @pytest.mark.parametrize("g", _cases("c3red") + _cases("c4red"))
@@ -73,7 +102,7 @@ def test_3d_configs_first_iterations_at_size(g):
         finally:
             os.environ.pop("FFTC_LEAN", None)
         check(rl, g)
-        assert [(h.sigma_star, h.residual) for h in rl.history] == [(h.sigma_star, h.residual) for h in r.history]
+        _same_to_roundoff(r, rl)
 
 
 def _lean_pair(chi, sigma1, e0, max_iters, fields):
@@ -96,20 +125,15 @@ def _lean_pair(chi, sigma1, e0, max_iters, fields):
 
 
 @pytest.mark.parametrize("shape,frac,sigma1", [((256, 256, 512), 0.3, 50.0), ((256, 512, 512), 0.25, 20.0 + 3.0j)])
-def test_lean_em_sub_bit_identical(shape, frac, sigma1):
+def test_lean_em_sub_matches_normal_schedule(shape, frac, sigma1):
     """Compact S/T slots and the split flux / residual-field transforms change
-    where values live and the launch order, not the arithmetic: histories,
-    sigma*, <E>, <J> and the returned fields equal the normal schedule's bit
-    for bit."""
+    where values live, the launch order and the order of the flux sums, not
+    the per-element arithmetic: histories, sigma*, <E>, <J> and the returned
+    fields equal the normal schedule's to summation order."""
     rng = np.random.default_rng(3)
     chi = rng.random(shape) < frac
     a, b = _lean_pair(chi, sigma1, (0.6, 0.0, 0.8), 60, True)
-    assert (a.status, a.iterations) == (b.status, b.iterations)
-    assert [(h.sigma_star, h.residual) for h in a.history] == [(h.sigma_star, h.residual) for h in b.history]
-    assert np.array_equal(a.mean_E, b.mean_E) and np.array_equal(a.mean_J, b.mean_J)
-    for fa, fb_ in ((a.E_field, b.E_field), (a.J_field, b.J_field), (a.aug_field.S, b.aug_field.S),
-                    (a.aug_field.T, b.aug_field.T)):
-        assert np.array_equal(fa.data, fb_.data)
+    _same_to_roundoff(a, b, fields=True)
 
 
 def test_lean_em_sub_c3_converged():
@@ -119,5 +143,5 @@ def test_lean_em_sub_c3_converged():
     chi = np.zeros(n, dtype=bool)
     chi[48:208, 48:208, 96:416] = True
     a, b = _lean_pair(chi, 100.0, (1.0, 0.0, 0.0), 2000, False)
-    assert a.status.value == "Converged" and b.iterations == a.iterations
-    assert b.sigma_star == a.sigma_star and math.isfinite(abs(b.sigma_star))
+    assert a.status.value == "Converged" and math.isfinite(abs(b.sigma_star))
+    _same_to_roundoff(a, b)
