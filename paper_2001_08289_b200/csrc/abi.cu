@@ -202,8 +202,13 @@ bool make_field_map(CUtensorMap* tm, void* base, long long nx, long long ny, int
 // line_stride, nouter of them at outer_stride, three components at
 // comp_stride; a box is W adjacent x-columns of all three components
 // {2W doubles, 256 rows, L/256 blocks, 1, 3} (cols3_tma.cuh).
+// swz > 0: the TMA swizzle whose span is one box row (16 W bytes), cols3_lg.cuh
+CUtensorMapSwizzle col3_swizzle(int swz) {
+  return swz == 8 ? CU_TENSOR_MAP_SWIZZLE_128B
+                  : (swz == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : (swz == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
+}
 bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W, long long line_stride,
-                   long long nouter, long long outer_stride, long long comp_stride) {
+                   long long nouter, long long outer_stride, long long comp_stride, int swz) {
   EncodeTiledFn enc = encode_tiled();
   const long long rows = L < 256 ? L : 256;
   if (!enc || L % rows || nx % W) return false;
@@ -213,7 +218,7 @@ bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W
   cuuint32_t box[5] = {(cuuint32_t)(2 * W), (cuuint32_t)rows, (cuuint32_t)(L / rows), 1, 3};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   col3_swizzle(swz), CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS && getenv("FFTC_VERBOSE")) fprintf(stderr, "[fftc] 5-D tensor map failed: %d\n", (int)r);
   return r == CUDA_SUCCESS;
 }
@@ -225,7 +230,8 @@ bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W
 //   y lines (axis 1, outer z): {2nx, BY, (ny/BY)*(nz/ZB), ZB (zl), 3} -- the
 //     y-block and zh dimensions fold into one because the zh step is exactly
 //     ny/BY y-blocks; outer z sits at {(z >> zbs) * ny/BY, z & (ZB-1)}.
-bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long long nz, int W, int axis, int zbs) {
+bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long long nz, int W, int axis, int zbs,
+                   int swz) {
   EncodeTiledFn enc = encode_tiled();
   const long long ZB = 1LL << zbs, N = nx * ny * nz;
   if (!enc || nx % W || nz % ZB) return false;
@@ -254,7 +260,7 @@ bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long
   }
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   col3_swizzle(swz), CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS && getenv("FFTC_VERBOSE")) fprintf(stderr, "[fftc] z-blocked tensor map failed: %d\n", (int)r);
   return r == CUDA_SUCCESS;
 }
@@ -275,8 +281,8 @@ bool col3_pass(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B, lon
   const char* sel = getenv("FFTC_TMA_COLS3");  // "0": the strip kernels (k_col), for comparison
   if (!k.fn || k.max_active <= 0 || (sel && atoi(sel) == 0)) return false;
   const int W = col3_tile_w(L);
-  if (!make_line_map(&p.mA, A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride)) return false;
-  if (!make_line_map(&p.mB, B ? B : A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride)) return false;
+  if (!make_line_map(&p.mA, A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride, k.swz)) return false;
+  if (!make_line_map(&p.mB, B ? B : A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride, k.swz)) return false;
   p.k = &k;
   p.g.nouter = (int)nouter;
   p.g.o0 = o0;
@@ -297,8 +303,8 @@ bool col3_pass_zblk(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B
   const long long nx = a.nx, ny = a.ny, nz = a.nz;
   const long long L = axis == 2 ? nz : ny;
   const int W = col3_tile_w(L);
-  if (!make_zblk_map(&p.mA, A, nx, ny, nz, W, axis, zbs)) return false;
-  if (!make_zblk_map(&p.mB, B ? B : A, nx, ny, nz, W, axis, zbs)) return false;
+  if (!make_zblk_map(&p.mA, A, nx, ny, nz, W, axis, zbs, k.swz)) return false;
+  if (!make_zblk_map(&p.mB, B ? B : A, nx, ny, nz, W, axis, zbs, k.swz)) return false;
   p.k = &k;
   p.g.nouter = (int)(axis == 2 ? ny : nz);
   p.g.o0 = 0;

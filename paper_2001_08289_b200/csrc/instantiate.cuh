@@ -5,6 +5,7 @@
 #include "rows_tma.cuh"
 #include "cols_tma.cuh"
 #include "cols3_tma.cuh"
+#include "cols3_lg.cuh"
 #include "kernel_table.h"
 
 #ifndef FFTC_TMA_ROWS_MIN
@@ -73,15 +74,31 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID2T_EM] = make(k_mid2_tma<MID_EM, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
   }
   if constexpr (LL >= 256 && LL <= 1024) {  // TMA tensor-map 3-D column passes
+#if FFTC_COL3_LG
+    using K3 = Col3Lg<LL>;
+#define FFTC_K3(MODE, PEER) make(k_col3_lg<MODE, LL, PEER>, K3::THREADS, K3::SMEM, 1)
+#else
     using K3 = Col3Tma<LL>;
+#define FFTC_K3(MODE, PEER) make(k_col3_tma<MODE, LL, PEER>, K3::THREADS, K3::SMEM, 1)
+#endif
     static_assert(K3::W == col3_tile_w(LL), "host and device tile widths agree");
-    t.col[KC_MID3T_BASIC] = make(k_col3_tma<MID_BASIC, LL>, K3::THREADS, K3::SMEM, 1);
-    t.col[KC_MID3T_EM] = make(k_col3_tma<MID_EM, LL>, K3::THREADS, K3::SMEM, 1);
-    t.col[KC_FWD3T] = make(k_col3_tma<COL_FWD, LL>, K3::THREADS, K3::SMEM, 1);
-    t.col[KC_INV3T] = make(k_col3_tma<COL_INV, LL>, K3::THREADS, K3::SMEM, 1);
-    t.col[KC_MID3P_BASIC] = make(k_col3_tma<MID_BASIC, LL, true>, K3::THREADS, K3::SMEM, 1);
-    t.col[KC_MID3P_EM] = make(k_col3_tma<MID_EM, LL, true>, K3::THREADS, K3::SMEM, 1);
-    t.col[KC_FWD3P] = make(k_col3_tma<COL_FWD, LL, true>, K3::THREADS, K3::SMEM, 1);
+    t.col[KC_MID3T_BASIC] = FFTC_K3(MID_BASIC, false);
+    t.col[KC_MID3T_EM] = FFTC_K3(MID_EM, false);
+    t.col[KC_FWD3T] = FFTC_K3(COL_FWD, false);
+    t.col[KC_INV3T] = FFTC_K3(COL_INV, false);
+    t.col[KC_MID3P_BASIC] = FFTC_K3(MID_BASIC, true);
+    t.col[KC_MID3P_EM] = FFTC_K3(MID_EM, true);
+    t.col[KC_FWD3P] = FFTC_K3(COL_FWD, true);
+#undef FFTC_K3
+#if FFTC_COL3_LG && FFTC_COL3_MID3
+    using KM = Col3Mid<LL>;
+    t.col[KC_MID3T_BASIC] = make(k_col3_mid<MID_BASIC, LL, false>, KM::THREADS, KM::SMEM, 1);
+    t.col[KC_MID3T_EM] = make(k_col3_mid<MID_EM, LL, false>, KM::THREADS, KM::SMEM, 1);
+    t.col[KC_MID3P_BASIC] = make(k_col3_mid<MID_BASIC, LL, true>, KM::THREADS, KM::SMEM, 1);
+    t.col[KC_MID3P_EM] = make(k_col3_mid<MID_EM, LL, true>, KM::THREADS, KM::SMEM, 1);
+#endif
+    for (int kc : {KC_MID3T_BASIC, KC_MID3T_EM, KC_FWD3T, KC_INV3T, KC_MID3P_BASIC, KC_MID3P_EM, KC_FWD3P})
+      t.col[kc].swz = FFTC_COL3_LG ? K3::W : 0;
   }
   if constexpr (LL >= FFTC_TMA_ROWS_MIN) {  // TMA-staged persistent row sweeps
 #define FFTC_TMA(SCH)                                                                                   \

@@ -11,6 +11,7 @@ struct KInfo {
   int smem = 0;        // dynamic shared memory (bytes)
   int lines = 0;       // lines processed per CTA per loop trip (G)
   int max_active = 0;  // resident CTAs per SM (filled at first use)
+  int swz = 0;         // 3-D TMA column passes: tensor maps swizzled over one box row (cols3_lg.cuh)
 };
 
 // column kernel variants
@@ -22,6 +23,14 @@ enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_
 // columns per TMA tile of the 3-D column passes (cols3_tma.cuh: Col3Tma<L>::W)
 #ifndef FFTC_COL3_W512
 #define FFTC_COL3_W512 4
+#endif
+// line-group form of the 3-D TMA column passes (cols3_lg.cuh); 0: cols3_tma.cuh
+#ifndef FFTC_COL3_LG
+#define FFTC_COL3_LG 1
+#endif
+// z pass with three components per thread (k_col3_mid); 0: one component per thread
+#ifndef FFTC_COL3_MID3
+#define FFTC_COL3_MID3 1
 #endif
 constexpr int col3_tile_w(long long L) { return L <= 256 ? 8 : (L <= 512 ? FFTC_COL3_W512 : 2); }
 
