@@ -598,6 +598,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
   a.nz = (int)nz;
   a.N = N;
   a.chi = pb->chi;
+  a.row_e = row_e((int)nx, (int)scheme);
   fill_scalars(a, pr, d, N);
 
   // ---- workspace ----
@@ -756,12 +757,12 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
       if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) break;
       if (lean) {  // rank codes of the compact S/T slots
-        void* ra[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiR};
+        void* ra[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiR, (void*)&a.row_e};
         if ((rc = Lc.raw((const void*)k_chi_rank16, g, 256, 0, ra, K_INIT))) break;
       } else if (chi_perm) {
-        const long long chunks = rows * (nx / 16);
+        const long long chunks = rows * (nx / a.row_e);
         unsigned gp = (unsigned)std::min<long long>((chunks + 255) / 256, (long long)R.num_sms * 16);
-        void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT};
+        void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT, (void*)&a.row_e};
         if ((rc = Lc.raw((const void*)k_chi_perm16, gp, 256, 0, pa, K_INIT))) break;
       }
     }
@@ -1541,6 +1542,7 @@ int fftc_slab_create(const fftc_slab_desc* sd, const fftc_params* pr, void* Az, 
   a.nz = (int)sd->nzl;
   a.N = N_l;
   a.chi = sd->chi;
+  a.row_e = row_e((int)nx, (int)pr->scheme);
   fill_scalars(a, pr, d, N_g);  // means and normalisations are global
   a.dist = 1;
   const int nslots = pr->scheme == FFTC_EM_SUB ? 3 : (pr->scheme == FFTC_BASIC_SUB ? 2 : 1);
@@ -1642,9 +1644,9 @@ int fftc_slab_phase(fftc_slab* sl, int32_t phase, double* out, void* stream) {
       void* ea[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.row_ext};
       if ((rc = Lc.raw((const void*)k_row_extent, g, 256, 0, ea, K_INIT))) return rc;
       if (a.chiT) {
-        const long long chunks = rows * (a.nx / 16);
+        const long long chunks = rows * (a.nx / a.row_e);
         unsigned gp = (unsigned)std::min<long long>((chunks + 255) / 256, (long long)R.num_sms * 16);
-        void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT};
+        void* pa[] = {(void*)&a.chi, (void*)&a.nx, (void*)&rows, (void*)&a.chiT, (void*)&a.row_e};
         if ((rc = Lc.raw((const void*)k_chi_perm16, gp, 256, 0, pa, K_INIT))) return rc;
       }
       switch (sl->scheme) {

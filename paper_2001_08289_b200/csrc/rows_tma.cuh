@@ -21,8 +21,13 @@ namespace fftc {
 #define FFTC_ST_NSTAGE 1
 #endif
 
-#ifndef FFTC_ROW_E
-#define FFTC_ROW_E 16
+// resident CTAs per SM the 8-per-thread rows of 512 size their registers for
+// (sweep 1: 64 threads per channel; sweep 3: 64 threads per CTA)
+#ifndef FFTC_ROW512_MINB1
+#define FFTC_ROW512_MINB1 4
+#endif
+#ifndef FFTC_ROW512_MINB3
+#define FFTC_ROW512_MINB3 8
 #endif
 // Variant V of the em_sub row sweeps for the memory-lean schedule (abi.cu,
 // compact S/T slots, one work field): 0 = the normal sweeps; 1 = sweep 1 of
@@ -31,7 +36,7 @@ namespace fftc {
 // voxel) instead of phase flags.
 template <int S, int SW, int L, int V = 0>
 struct RowTma {
-  static constexpr int E = FFTC_ROW_E;
+  static constexpr int E = row_e(L, S);  // 16, or 8 on rows of 512 of the substituted schemes (sweeps.cuh)
   static constexpr int T = L / E;
   static constexpr bool LEAN = V != 0;
   static constexpr int CH = (SW == 1 && !LEAN) ? Sweep1Traits<S>::C : 1;
@@ -78,7 +83,8 @@ struct RowTma {
   // 5.78 ms, so those keep the tuned values)
   static constexpr int MINB_TUNED = SW == 3 ? 3 : (ST_ROWS ? 1 : 2);
   static constexpr int MINB_FILL = (232448 / (SMEM + 1024)) < (512 / THREADS) ? (232448 / (SMEM + 1024)) : (512 / THREADS);
-  static constexpr int MINB = (L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1);
+  static constexpr int MINB_E8 = SW == 3 ? FFTC_ROW512_MINB3 : (CH == 2 ? FFTC_ROW512_MINB1 : 2 * FFTC_ROW512_MINB1);
+  static constexpr int MINB = E == 8 ? MINB_E8 : ((L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1));
 };
 
 template <int S, int SW, int L, int V = 0>
@@ -114,44 +120,63 @@ __device__ __forceinline__ void rows_tma_issue(const Args& a, double2* stage, ui
     bulk_g2s(stage + K::CHI_OFF, a.chiT + (size_t)row * L, (unsigned)L, bar);  // thread-blocked chi row
 }
 
-// a thread's 16 phase flags (chiT row bytes t*16 .. t*16+15, element i = byte i)
-struct ChiBytes16 {
-  uint32_t w[4];
+// a thread's E phase flags (chiT row bytes t*E .. t*E+E-1, element i = byte i)
+template <int E>
+struct ChiBytes {
+  uint32_t w[E / 4];
   __device__ __forceinline__ bool in1(int i) const { return ((w[i >> 2] >> ((i & 3) << 3)) & 0xffu) != 0u; }
 };
-__device__ __forceinline__ ChiBytes16 load_chi16(const uint8_t* chi_s, int t) {
-  const uint4 c = *reinterpret_cast<const uint4*>(chi_s + 16 * t);
-  return ChiBytes16{{c.x, c.y, c.z, c.w}};
+template <int E>
+__device__ __forceinline__ ChiBytes<E> load_chi(const uint8_t* chi_s, int t) {
+  static_assert(E == 8 || E == 16, "thread-blocked chi rows hold 8 or 16 flags per thread");
+  ChiBytes<E> r;
+  if constexpr (E == 16) {
+    const uint4 c = *reinterpret_cast<const uint4*>(chi_s + 16 * t);
+    r.w[0] = c.x; r.w[1] = c.y; r.w[2] = c.z; r.w[3] = c.w;
+  } else {
+    const uint2 c = *reinterpret_cast<const uint2*>(chi_s + 8 * t);
+    r.w[0] = c.x; r.w[1] = c.y;
+  }
+  return r;
 }
 
-// a thread's 16 rank codes of the compact layout (chiR row entries t*16 ..
-// t*16+15): element i is phase 1 when its code is nonzero, and its S/T slot
+// a thread's E rank codes of the compact layout (chiR row entries t*E ..
+// t*E+E-1): element i is phase 1 when its code is nonzero, and its S/T slot
 // is the row's compact base + code - 1
-struct ChiCodes16 {
-  uint32_t w[8];
+template <int E>
+struct ChiCodes {
+  uint32_t w[E / 2];
   __device__ __forceinline__ int code(int i) const { return (int)((w[i >> 1] >> ((i & 1) << 4)) & 0xffffu); }
   __device__ __forceinline__ bool in1(int i) const { return code(i) != 0; }
 };
-__device__ __forceinline__ ChiCodes16 load_codes16(const uint8_t* chi_s, int t) {
-  const uint4 c0 = *reinterpret_cast<const uint4*>(chi_s + 32 * t);
-  const uint4 c1 = *reinterpret_cast<const uint4*>(chi_s + 32 * t + 16);
-  return ChiCodes16{{c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w}};
+template <int E>
+__device__ __forceinline__ ChiCodes<E> load_codes(const uint8_t* chi_s, int t) {
+  ChiCodes<E> r;
+  const uint4 c0 = *reinterpret_cast<const uint4*>(chi_s + 2 * E * t);
+  r.w[0] = c0.x; r.w[1] = c0.y; r.w[2] = c0.z; r.w[3] = c0.w;
+  if constexpr (E == 16) {
+    const uint4 c1 = *reinterpret_cast<const uint4*>(chi_s + 32 * t + 16);
+    r.w[4] = c1.x; r.w[5] = c1.y; r.w[6] = c1.z; r.w[7] = c1.w;
+  }
+  return r;
 }
-template <bool LEAN>
+template <bool LEAN, int E>
 struct PhaseRow;
-template <>
-struct PhaseRow<false> {
-  using type = ChiBytes16;
-  static __device__ __forceinline__ ChiBytes16 load(const uint8_t* chi_s, int t) { return load_chi16(chi_s, t); }
+template <int E>
+struct PhaseRow<false, E> {
+  using type = ChiBytes<E>;
+  static __device__ __forceinline__ type load(const uint8_t* chi_s, int t) { return load_chi<E>(chi_s, t); }
 };
-template <>
-struct PhaseRow<true> {
-  using type = ChiCodes16;
-  static __device__ __forceinline__ ChiCodes16 load(const uint8_t* chi_s, int t) { return load_codes16(chi_s, t); }
+template <int E>
+struct PhaseRow<true, E> {
+  using type = ChiCodes<E>;
+  static __device__ __forceinline__ type load(const uint8_t* chi_s, int t) { return load_codes<E>(chi_s, t); }
 };
 // S/T slot of element i of this thread: full-grid (off + x) or compact (base + code - 1)
-__device__ __forceinline__ size_t st_slot(const ChiBytes16&, int, size_t off, int x) { return off + x; }
-__device__ __forceinline__ size_t st_slot(const ChiCodes16& cc, int i, size_t base, int) {
+template <int E>
+__device__ __forceinline__ size_t st_slot(const ChiBytes<E>&, int, size_t off, int x) { return off + x; }
+template <int E>
+__device__ __forceinline__ size_t st_slot(const ChiCodes<E>& cc, int i, size_t base, int) {
   return base + (size_t)(cc.code(i) - 1);
 }
 
@@ -193,7 +218,7 @@ __device__ __forceinline__ void rows_tma_prefetch_slots(const Args& a, int line,
 // exchange buffer; each position is read and rewritten by one thread only).
 template <int H, int L, int E, int NQ>
 __device__ __forceinline__ void em_sub_prologue_half(const Args& a, double2 (&v)[1][E], const double2* st,
-                                                     const ChiBytes16& cb, double2* other, int t, int c, size_t off,
+                                                     const ChiBytes<E>& cb, double2* other, int t, int c, size_t off,
                                                      double2 dl, double (&acc)[NQ]) {
   // S/T loads (phase 1 only, L2-prefetched) in batches of NB issued ahead of
   // the batch's staging stores; interleaved with them each would wait one latency
@@ -277,7 +302,6 @@ __global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L,
     const double2 dl = sdelta[c];
     double2* st = smem + s * K::STAGE;
     const uint8_t* chi_s = reinterpret_cast<const uint8_t*>(st + K::CHI_OFF);
-    static_assert(E == 16, "the thread-blocked chi rows (k_chi_perm16) hold 16 flags per thread");
     if (pf) {
       const int2 ext = ext_next;
       const int l2 = line + 2 * (int)gridDim.x;
@@ -285,7 +309,7 @@ __global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L,
       rows_tma_prefetch_slots<S, SW, L, V>(a, line + (int)gridDim.x, lines, rows, ext);
     }
     mbar_wait(&bars[s], parity);
-    const typename PhaseRow<K::LEAN>::type cb = PhaseRow<K::LEAN>::load(chi_s, t);
+    const typename PhaseRow<K::LEAN, E>::type cb = PhaseRow<K::LEAN, E>::load(chi_s, t);
     // S/T slot base of this line: the full-grid row, or the row's compact run
     const size_t sbase = K::LEAN ? (size_t)c * a.M + (size_t)a.rowoff[row] : off;
     double2 v[1][E];

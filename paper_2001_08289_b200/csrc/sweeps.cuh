@@ -69,6 +69,7 @@ struct Args {
   // byte t*16 + i holds chi[t + i*nx/16], so a thread's 16 phase flags are one
   // 16-byte shared-memory load (k_chi_perm16)
   const uint8_t* chiT;
+  int row_e;  // elements per thread of that order: row_e(nx, scheme), 16 or 8
   // Compact S/T slots (the memory-lean em_sub schedule, abi.cu): when rowoff
   // is set, X[1] and X[2] hold only the phase-1 voxels -- row r's, in x
   // order, at [rowoff[r], rowoff[r+1]) of each component's block of M --
@@ -112,11 +113,25 @@ struct Args {
   double2 cinv_p1, cinv_p2, cinv_p3;  // ((t-1)/(t+s0)) p_i
 };
 
+// Elements per thread of the TMA row sweeps on rows of length L, scheme S
+// (rows_tma.cuh): 16 (radix-16 stages), except rows of 512 = 8 x 8 x 8 of the
+// substituted schemes, where 8 per thread costs the same two exchanges as
+// 16 x 2 x 16 and twice the warps fit an SM.  Measured at 512^3 (8 vs 16, ms):
+// em_sub sweep 1 5.31 / 5.39, sweep 3 3.25 / 3.70; basic_sub 2.94 / 2.75 and
+// 3.12 / 3.40; basic sweep 1 2.50 / 2.30 and em 4.87 / 4.58 (already near the
+// HBM rate with 16), so basic and em keep 16.  FFTC_ROW_E512 = 16 switches it off.
+#ifndef FFTC_ROW_E512
+#define FFTC_ROW_E512 8
+#endif
+__host__ __device__ constexpr int row_e(int L, int S) {
+  return (L == 512 && (S == 2 || S == 3)) ? FFTC_ROW_E512 : 16;  // (S: BASIC_SUB = 2, EM_SUB = 3)
+}
+
 // index of voxel (row, x) in the thread-blocked row order of chiT / chiR
-// (16 elements per thread: x = t + i*nx/16 sits at 16 t + i)
-__device__ __forceinline__ long long tblock_index(long long row, int x, int nx) {
-  const int T = nx >> 4;
-  return row * nx + 16 * (x % T) + x / T;
+// (E = Args::row_e elements per thread: x = t + i*nx/E sits at E t + i)
+__device__ __forceinline__ long long tblock_index(long long row, int x, int nx, int E) {
+  const int T = nx / E;
+  return row * nx + E * (x % T) + x / T;
 }
 
 // compact S/T slot of voxel p = row*nx + x, component c (lean layout), or -1
@@ -124,7 +139,7 @@ __device__ __forceinline__ long long tblock_index(long long row, int x, int nx) 
 __device__ __forceinline__ long long compact_slot(const Args& a, int c, long long p) {
   const long long row = p / a.nx;
   const int x = (int)(p - row * a.nx);
-  const int code = a.chiR[tblock_index(row, x, a.nx)];
+  const int code = a.chiR[tblock_index(row, x, a.nx, a.row_e)];
   return code ? (long long)c * a.M + a.rowoff[row] + (code - 1) : -1;
 }
 
@@ -809,11 +824,11 @@ static __global__ void __launch_bounds__(256) k_row_extent(const uint8_t* __rest
 }
 
 // chi rows -> the thread-blocked order of the row sweeps (Args::chiT): one
-// thread per 16-byte output chunk (row r, thread slot t) gathers the 16 bytes
-// chi[r][t + i*T], i = 0..15, T = nx/16 (consecutive t read consecutive bytes)
+// thread per E-byte output chunk (row r, thread slot t) gathers the E bytes
+// chi[r][t + i*T], i = 0..E-1, T = nx/E (consecutive t read consecutive bytes)
 static __global__ void __launch_bounds__(256) k_chi_perm16(const uint8_t* __restrict__ chi, int nx, long long rows,
-                                                          uint8_t* __restrict__ out) {
-  const int T = nx >> 4;
+                                                          uint8_t* __restrict__ out, int E) {
+  const int T = nx / E;  // (E = 16 or 8: Args::row_e)
   const long long n = rows * T;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -823,9 +838,12 @@ static __global__ void __launch_bounds__(256) k_chi_perm16(const uint8_t* __rest
     uint32_t w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      w[k] = (uint32_t)(src[(4 * k) * T] != 0) | ((uint32_t)(src[(4 * k + 1) * T] != 0) << 8) |
-             ((uint32_t)(src[(4 * k + 2) * T] != 0) << 16) | ((uint32_t)(src[(4 * k + 3) * T] != 0) << 24);
-    *reinterpret_cast<uint4*>(out + (size_t)r * nx + 16 * t) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (4 * k < E)
+        w[k] = (uint32_t)(src[(4 * k) * T] != 0) | ((uint32_t)(src[(4 * k + 1) * T] != 0) << 8) |
+               ((uint32_t)(src[(4 * k + 2) * T] != 0) << 16) | ((uint32_t)(src[(4 * k + 3) * T] != 0) << 24);
+    uint8_t* dst = out + (size_t)r * nx + (size_t)E * t;
+    if (E == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    else *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
   }
 }
 
@@ -848,7 +866,7 @@ static __global__ void __launch_bounds__(256) k_row_counts(const uint8_t* __rest
 // scans x in [l*nx/32, (l+1)*nx/32) in order after a warp prefix sum of the
 // lanes' counts; codes land in the thread-blocked order of chiT
 static __global__ void __launch_bounds__(256) k_chi_rank16(const uint8_t* __restrict__ chi, int nx, long long rows,
-                                                         uint16_t* __restrict__ out) {
+                                                         uint16_t* __restrict__ out, int E) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -867,7 +885,7 @@ static __global__ void __launch_bounds__(256) k_chi_rank16(const uint8_t* __rest
     int rank = incl - n;
     for (int x = x0; x < x1; ++x) {
       const bool in1 = row[x] != 0;
-      out[tblock_index(r, x, nx)] = in1 ? (uint16_t)(rank + 1) : (uint16_t)0;
+      out[tblock_index(r, x, nx, E)] = in1 ? (uint16_t)(rank + 1) : (uint16_t)0;
       rank += in1;
     }
   }
