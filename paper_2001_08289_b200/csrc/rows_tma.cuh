@@ -29,6 +29,14 @@ namespace fftc {
 #ifndef FFTC_ROW512_MINB3
 #define FFTC_ROW512_MINB3 8
 #endif
+// em_sub sweep 1 on 8-per-thread rows: both channels (Rq, Jq) in one thread
+// (1), or split over two thread groups with a shared-memory handoff (0)
+#ifndef FFTC_ROW512_CPT2
+#define FFTC_ROW512_CPT2 1
+#endif
+#ifndef FFTC_ROW512_MINBC
+#define FFTC_ROW512_MINBC 6
+#endif
 // Variant V of the em_sub row sweeps for the memory-lean schedule (abi.cu,
 // compact S/T slots, one work field): 0 = the normal sweeps; 1 = sweep 1 of
 // the flux channel Jq alone; 2 = sweep 1 of the residual field Rq alone;
@@ -39,7 +47,12 @@ struct RowTma {
   static constexpr int E = row_e(L, S);  // 16, or 8 on rows of 512 of the substituted schemes (sweeps.cuh)
   static constexpr int T = L / E;
   static constexpr bool LEAN = V != 0;
-  static constexpr int CH = (SW == 1 && !LEAN) ? Sweep1Traits<S>::C : 1;
+  // channels carried by one thread: em_sub's two sweep-1 channels on
+  // 8-per-thread rows (16 values per thread, as one channel of 16): the
+  // prologue runs once per element with no handoff between thread groups,
+  // and one set of twiddle powers serves both transforms
+  static constexpr int CPT = (FFTC_ROW512_CPT2 && SW == 1 && !LEAN && S == EM_SUB && E == 8) ? 2 : 1;
+  static constexpr int CH = (SW == 1 && !LEAN && CPT == 1) ? Sweep1Traits<S>::C : 1;
   static constexpr int THREADS = CH * T;
   static constexpr bool X0_ROW = (SW == 3) && (S == BASIC || S == BASIC_SUB);  // extra staged row
   // sweep 1 of the substituted schemes also stages its S (and T) rows over
@@ -71,7 +84,7 @@ struct RowTma {
                               ((SW == 1 && ST_ROWS == 0) ||
                                (SW == 3 && (S == BASIC || S == BASIC_SUB)) || (SW == 3 && S == EM_SUB && L >= 2048));
   static constexpr int NSTAGE = TWS ? 1 : (ST_ROWS ? FFTC_ST_NSTAGE : 2);
-  static constexpr int XBUF = (CH == 2 && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
+  static constexpr int XBUF = ((CH == 2 || CPT == 2) && ST_ROWS == 0) ? LP : 0;  // exchange buffer of channel 1
   static constexpr int TWOFF = NSTAGE * STAGE + XBUF;              // double2 units
   static constexpr int SMEM = (TWOFF + (TWS ? L / 2 : 0)) * (int)sizeof(double2);
   static constexpr unsigned TX = (unsigned)(L * sizeof(double2) * (1 + (X0_ROW ? 1 : 0)) + CHI_BYTES);
@@ -83,7 +96,8 @@ struct RowTma {
   // 5.78 ms, so those keep the tuned values)
   static constexpr int MINB_TUNED = SW == 3 ? 3 : (ST_ROWS ? 1 : 2);
   static constexpr int MINB_FILL = (232448 / (SMEM + 1024)) < (512 / THREADS) ? (232448 / (SMEM + 1024)) : (512 / THREADS);
-  static constexpr int MINB_E8 = SW == 3 ? FFTC_ROW512_MINB3 : (CH == 2 ? FFTC_ROW512_MINB1 : 2 * FFTC_ROW512_MINB1);
+  static constexpr int MINB_E8 =
+      SW == 3 ? FFTC_ROW512_MINB3 : (CPT == 2 ? FFTC_ROW512_MINBC : (CH == 2 ? FFTC_ROW512_MINB1 : 2 * FFTC_ROW512_MINB1));
   static constexpr int MINB = E == 8 ? MINB_E8 : ((L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1));
 };
 
@@ -312,9 +326,36 @@ __global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L,
     const typename PhaseRow<K::LEAN, E>::type cb = PhaseRow<K::LEAN, E>::load(chi_s, t);
     // S/T slot base of this line: the full-grid row, or the row's compact run
     const size_t sbase = K::LEAN ? (size_t)c * a.M + (size_t)a.rowoff[row] : off;
-    double2 v[1][E];
+    constexpr int CPT = K::CPT;
+    double2 v[CPT][E];
     constexpr bool SPLIT = (SW == 1 && S == EM_SUB && CH == 2 && K::ST_ROWS == 0);
-    if constexpr (SPLIT) {
+    if constexpr (CPT == 2) {
+      // ---- em_sub prologue, both channels in this thread (solvers.py:398-420):
+      // channel 0 = Rq, channel 1 = Jq; S/T loads of the whole thread first ----
+      double2 sv[E], tv[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        sv[i] = tv[i] = czero();
+        if (cb.in1(i)) {
+          const int x = pos_first<L, E>(false, t, i);
+          sv[i] = a.X[1][st_slot(cb, i, sbase, x)];
+          tv[i] = a.X[2][st_slot(cb, i, sbase, x)];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int x = pos_first<L, E>(false, t, i);
+        const bool in1 = cb.in1(i);
+        const double2 q = st[x];
+        const AugFlux f = apply_A(a, in1, q, sv[i], tv[i]);
+        double2 jq, js;
+        pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
+        acc_c<NQ>(acc, c, jq);
+        if (in1) acc[NQ - 1] += cabs2(js);
+        v[0][i] = csub(f.jq, cmul(a.s0, q));
+        v[1][i] = jq;
+      }
+    } else if constexpr (SPLIT) {
       // ---- prologue, each element once (see em_sub_prologue_half) ----
       if (ch == 0) em_sub_prologue_half<0, L, E, NQ>(a, v, st, cb, xbuf, t, c, off, dl, acc);
       else em_sub_prologue_half<1, L, E, NQ>(a, v, st, cb, st, t, c, off, dl, acc);
@@ -376,7 +417,13 @@ __global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L,
       }
       HalfSync{1 + ch, T}();  // every staged value is read before the first exchange overwrites it
     }
-    if constexpr (CH == 2) {
+    if constexpr (CPT == 2) {
+      // both channels through one transform (shared twiddle powers): channel 0
+      // exchanges in the main row, channel 1 in xbuf
+      const SmemBuf xb2{st, (int)(xbuf - st)};
+      if constexpr (K::TWS) fft_line<L, E, 2, INV, false>(v, t, SmemTw{smem + K::TWOFF}, xb2, SyncAll{});
+      else fft_line<L, E, 2, INV, false>(v, t, a.tw[0], xb2, SyncAll{});
+    } else if constexpr (CH == 2) {
       // the two channels transform in separate buffers: each synchronises
       // only its own T threads (named barrier 1 + ch), not the whole CTA
       // (no barrier after the last exchange: the __syncthreads closing the
@@ -395,6 +442,10 @@ __global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L,
       const size_t woff = work_off(a, c, row);  // work field row (z-blocked in 3-D)
 #pragma unroll
       for (int i = 0; i < E; ++i) OUT[woff + pos_last<L, E>(false, t, i)] = v[0][i];
+      if constexpr (CPT == 2) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) a.B[woff + pos_last<L, E>(false, t, i)] = v[1][i];
+      }
     } else {
       // ---- epilogue: state update for iteration k+1 (solvers.py:303-308, :398-411) ----
       // Elements go in batches of NB: the batch's phase-1 state loads (L2-
