@@ -37,6 +37,17 @@ namespace fftc {
 #ifndef FFTC_ROW512_MINBC
 #define FFTC_ROW512_MINBC 6
 #endif
+// The same for em (16-per-thread rows, 32 values per thread).  Measured, split
+// groups -> one thread (us): em at 2048^2 115.6 -> 111.5, at 512^3 4602 ->
+// 3789, but at 1024^2 35.3 -> 37.0, so rows of 1024 keep the split; em_sub on
+// 16-per-thread rows loses (2048^2 134.3 -> 142.5, 1024^2 38.9 -> 43.0: its
+// prologue needs the registers) and keeps the split there.
+#ifndef FFTC_ROW_CPT2_EM
+#define FFTC_ROW_CPT2_EM 1
+#endif
+#ifndef FFTC_ROW_CPT2_MINB16
+#define FFTC_ROW_CPT2_MINB16 2
+#endif
 // Variant V of the em_sub row sweeps for the memory-lean schedule (abi.cu,
 // compact S/T slots, one work field): 0 = the normal sweeps; 1 = sweep 1 of
 // the flux channel Jq alone; 2 = sweep 1 of the residual field Rq alone;
@@ -51,7 +62,10 @@ struct RowTma {
   // 8-per-thread rows (16 values per thread, as one channel of 16): the
   // prologue runs once per element with no handoff between thread groups,
   // and one set of twiddle powers serves both transforms
-  static constexpr int CPT = (FFTC_ROW512_CPT2 && SW == 1 && !LEAN && S == EM_SUB && E == 8) ? 2 : 1;
+  static constexpr int CPT = (SW == 1 && !LEAN &&
+                              ((S == EM_SUB && E == 8 && FFTC_ROW512_CPT2) || (S == EM && L != 1024 && FFTC_ROW_CPT2_EM)))
+                                 ? 2
+                                 : 1;
   static constexpr int CH = (SW == 1 && !LEAN && CPT == 1) ? Sweep1Traits<S>::C : 1;
   static constexpr int THREADS = CH * T;
   static constexpr bool X0_ROW = (SW == 3) && (S == BASIC || S == BASIC_SUB);  // extra staged row
@@ -98,7 +112,9 @@ struct RowTma {
   static constexpr int MINB_FILL = (232448 / (SMEM + 1024)) < (512 / THREADS) ? (232448 / (SMEM + 1024)) : (512 / THREADS);
   static constexpr int MINB_E8 =
       SW == 3 ? FFTC_ROW512_MINB3 : (CPT == 2 ? FFTC_ROW512_MINBC : (CH == 2 ? FFTC_ROW512_MINB1 : 2 * FFTC_ROW512_MINB1));
-  static constexpr int MINB = E == 8 ? MINB_E8 : ((L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1));
+  static constexpr int MINB = E == 8 ? MINB_E8
+                                     : (CPT == 2 ? FFTC_ROW_CPT2_MINB16
+                                                 : ((L != 1024 || SW == 3) ? MINB_TUNED : (MINB_FILL > 1 ? MINB_FILL : 1)));
 };
 
 template <int S, int SW, int L, int V = 0>
@@ -330,30 +346,45 @@ __global__ void __launch_bounds__(RowTma<S, SW, L, V>::THREADS, RowTma<S, SW, L,
     double2 v[CPT][E];
     constexpr bool SPLIT = (SW == 1 && S == EM_SUB && CH == 2 && K::ST_ROWS == 0);
     if constexpr (CPT == 2) {
-      // ---- em_sub prologue, both channels in this thread (solvers.py:398-420):
-      // channel 0 = Rq, channel 1 = Jq; S/T loads of the whole thread first ----
-      double2 sv[E], tv[E];
+      // ---- prologue, both channels in this thread (solvers.py:303-311 /
+      // :398-420): channel 0 = the residual field, channel 1 = the flux; the
+      // S/T loads of a batch are issued before its arithmetic ----
+      constexpr int NB = E == 8 ? 8 : 4;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        sv[i] = tv[i] = czero();
-        if (cb.in1(i)) {
-          const int x = pos_first<L, E>(false, t, i);
-          sv[i] = a.X[1][st_slot(cb, i, sbase, x)];
-          tv[i] = a.X[2][st_slot(cb, i, sbase, x)];
+      for (int b0 = 0; b0 < E; b0 += NB) {
+        double2 sv[NB], tv[NB];
+        if constexpr (S == EM_SUB) {
+#pragma unroll
+          for (int u = 0; u < NB; ++u) {
+            sv[u] = tv[u] = czero();
+            if (cb.in1(b0 + u)) {
+              const int x = pos_first<L, E>(false, t, b0 + u);
+              sv[u] = a.X[1][st_slot(cb, b0 + u, sbase, x)];
+              tv[u] = a.X[2][st_slot(cb, b0 + u, sbase, x)];
+            }
+          }
         }
-      }
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int x = pos_first<L, E>(false, t, i);
-        const bool in1 = cb.in1(i);
-        const double2 q = st[x];
-        const AugFlux f = apply_A(a, in1, q, sv[i], tv[i]);
-        double2 jq, js;
-        pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
-        acc_c<NQ>(acc, c, jq);
-        if (in1) acc[NQ - 1] += cabs2(js);
-        v[0][i] = csub(f.jq, cmul(a.s0, q));
-        v[1][i] = jq;
+        for (int u = 0; u < NB; ++u) {
+          const int i = b0 + u;
+          const int x = pos_first<L, E>(false, t, i);
+          const bool in1 = cb.in1(i);
+          const double2 q = st[x];
+          if constexpr (S == EM_SUB) {
+            const AugFlux f = apply_A(a, in1, q, sv[u], tv[u]);
+            double2 jq, js;
+            pinned_flux(a, in1, f.jq, f.js, dl, jq, js);
+            acc_c<NQ>(acc, c, jq);
+            if (in1) acc[NQ - 1] += cabs2(js);
+            v[0][i] = csub(f.jq, cmul(a.s0, q));
+            v[1][i] = jq;
+          } else {  // EM
+            const double2 j = cmul(sigma_at(a, in1), cadd(q, dl));
+            acc_c<NQ>(acc, c, j);
+            v[0][i] = cmul(in1 ? a.sm1 : a.sm2, q);
+            v[1][i] = j;
+          }
+        }
       }
     } else if constexpr (SPLIT) {
       // ---- prologue, each element once (see em_sub_prologue_half) ----
