@@ -208,14 +208,14 @@ CUtensorMapSwizzle col3_swizzle(int swz) {
                   : (swz == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : (swz == 2 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
 }
 bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W, long long line_stride,
-                   long long nouter, long long outer_stride, long long comp_stride, int swz) {
+                   long long nouter, long long outer_stride, long long comp_stride, int swz, int ncb = 3) {
   EncodeTiledFn enc = encode_tiled();
   const long long rows = L < 256 ? L : 256;
   if (!enc || L % rows || nx % W) return false;
   cuuint64_t dims[5] = {(cuuint64_t)(2 * nx), (cuuint64_t)rows, (cuuint64_t)(L / rows), (cuuint64_t)nouter, 3};
   cuuint64_t strides[4] = {(cuuint64_t)(line_stride * 16), (cuuint64_t)(line_stride * 16 * rows),
                            (cuuint64_t)(outer_stride * 16), (cuuint64_t)(comp_stride * 16)};
-  cuuint32_t box[5] = {(cuuint32_t)(2 * W), (cuuint32_t)rows, (cuuint32_t)(L / rows), 1, 3};
+  cuuint32_t box[5] = {(cuuint32_t)(2 * W), (cuuint32_t)rows, (cuuint32_t)(L / rows), 1, (cuuint32_t)ncb};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    col3_swizzle(swz), CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -231,7 +231,7 @@ bool make_line_map(CUtensorMap* tm, void* base, long long nx, long long L, int W
 //     y-block and zh dimensions fold into one because the zh step is exactly
 //     ny/BY y-blocks; outer z sits at {(z >> zbs) * ny/BY, z & (ZB-1)}.
 bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long long nz, int W, int axis, int zbs,
-                   int swz) {
+                   int swz, int ncb = 3) {
   EncodeTiledFn enc = encode_tiled();
   const long long ZB = 1LL << zbs, N = nx * ny * nz;
   if (!enc || nx % W || nz % ZB) return false;
@@ -242,7 +242,7 @@ bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long
     const cuuint64_t d5[5] = {(cuuint64_t)(2 * nx), (cuuint64_t)ZB, (cuuint64_t)(nz / ZB), (cuuint64_t)ny, 3};
     const cuuint64_t s4[4] = {(cuuint64_t)(nx * 16), (cuuint64_t)(ny * ZB * nx * 16), (cuuint64_t)(ZB * nx * 16),
                               (cuuint64_t)(N * 16)};
-    const cuuint32_t b5[5] = {(cuuint32_t)(2 * W), (cuuint32_t)ZB, (cuuint32_t)(nz / ZB), 1, 3};
+    const cuuint32_t b5[5] = {(cuuint32_t)(2 * W), (cuuint32_t)ZB, (cuuint32_t)(nz / ZB), 1, (cuuint32_t)ncb};
     memcpy(dims, d5, sizeof(dims));
     memcpy(strides, s4, sizeof(strides));
     memcpy(box, b5, sizeof(box));
@@ -253,7 +253,7 @@ bool make_zblk_map(CUtensorMap* tm, void* base, long long nx, long long ny, long
                               3};
     const cuuint64_t s4[4] = {(cuuint64_t)(ZB * nx * 16), (cuuint64_t)(BY * ZB * nx * 16), (cuuint64_t)(nx * 16),
                               (cuuint64_t)(N * 16)};
-    const cuuint32_t b5[5] = {(cuuint32_t)(2 * W), (cuuint32_t)BY, (cuuint32_t)(ny / BY), 1, 3};
+    const cuuint32_t b5[5] = {(cuuint32_t)(2 * W), (cuuint32_t)BY, (cuuint32_t)(ny / BY), 1, (cuuint32_t)ncb};
     memcpy(dims, d5, sizeof(dims));
     memcpy(strides, s4, sizeof(strides));
     memcpy(box, b5, sizeof(box));
@@ -280,16 +280,18 @@ bool col3_pass(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B, lon
   p.g = Line3{};
   const char* sel = getenv("FFTC_TMA_COLS3");  // "0": the strip kernels (k_col), for comparison
   if (!k.fn || k.max_active <= 0 || (sel && atoi(sel) == 0)) return false;
-  const int W = col3_tile_w(L);
-  if (!make_line_map(&p.mA, A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride, k.swz)) return false;
-  if (!make_line_map(&p.mB, B ? B : A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride, k.swz)) return false;
+  const int W = k.tile_w ? k.tile_w : col3_tile_w(L), ncb = k.tile_nc ? k.tile_nc : 3;
+  if (a.nx % W) return false;
+  if (!make_line_map(&p.mA, A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride, k.swz, ncb)) return false;
+  if (!make_line_map(&p.mB, B ? B : A, a.nx, L, W, line_stride, nouter, outer_stride, comp_stride, k.swz, ncb))
+    return false;
   p.k = &k;
   p.g.nouter = (int)nouter;
   p.g.o0 = o0;
   p.g.on = on;
   p.g.nfields = nfields;
   p.g.axis = axis;
-  p.tiles = nouter * (a.nx / W) * nfields;
+  p.tiles = nouter * (a.nx / W) * nfields * (3 / ncb);
   p.ok = true;
   return true;
 }
@@ -302,9 +304,10 @@ bool col3_pass_zblk(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B
   if (!k.fn || k.max_active <= 0 || (sel && atoi(sel) == 0)) return false;
   const long long nx = a.nx, ny = a.ny, nz = a.nz;
   const long long L = axis == 2 ? nz : ny;
-  const int W = col3_tile_w(L);
-  if (!make_zblk_map(&p.mA, A, nx, ny, nz, W, axis, zbs, k.swz)) return false;
-  if (!make_zblk_map(&p.mB, B ? B : A, nx, ny, nz, W, axis, zbs, k.swz)) return false;
+  const int W = k.tile_w ? k.tile_w : col3_tile_w(L), ncb = k.tile_nc ? k.tile_nc : 3;
+  if (nx % W) return false;
+  if (!make_zblk_map(&p.mA, A, nx, ny, nz, W, axis, zbs, k.swz, ncb)) return false;
+  if (!make_zblk_map(&p.mB, B ? B : A, nx, ny, nz, W, axis, zbs, k.swz, ncb)) return false;
   p.k = &k;
   p.g.nouter = (int)(axis == 2 ? ny : nz);
   p.g.o0 = 0;
@@ -313,7 +316,7 @@ bool col3_pass_zblk(Col3Pass& p, const KInfo& k, const Args& a, void* A, void* B
   p.g.axis = axis;
   p.g.obs = axis == 1 ? zbs : 0;
   p.g.om = axis == 1 ? (int)(ny / (ny < 256 ? ny : 256)) : 0;
-  p.tiles = (long long)p.g.nouter * (nx / W) * nfields;
+  p.tiles = (long long)p.g.nouter * (nx / W) * nfields * (3 / ncb);
   p.ok = true;
   return true;
 }
@@ -924,6 +927,12 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
         if (yfwd.ok) {
           void* ay[] = {&a, &yfwd.g, &yfwd.mA, &yfwd.mB, &no_peer};
           if ((r = L.go(*yfwd.k, yfwd.tiles, ay, K_YFWD))) return r;
+          // timing experiments only (results wrong): the pass once more right after
+          // itself (1), or the inverse-pass kernel on the same tiles (2)
+          if (const char* e = getenv("FFTC_DBG_YFWD2")) {
+            const KInfo& kk = atoi(e) == 2 ? TY.col[KC_INV3T] : *yfwd.k;
+            if ((r = L.go(kk, yfwd.tiles, ay, K_PARSEVAL))) return r;
+          }
         } else {
           Args aB = a;
           void* ayf[] = {&a, &yf};

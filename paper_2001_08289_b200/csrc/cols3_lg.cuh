@@ -54,19 +54,21 @@ __device__ __forceinline__ void col3_prefetch(const CUtensorMap* tm, int x0, int
                : "memory");
 }
 
-template <int L>
+// NCT components per tile (3: the projection pass needs them together; 1: the
+// plain y passes may take them one at a time), WT columns per tile, NS slots
+template <int L, int NCT = 3, int WT = col3_tile_w(L), int NS = 2>
 struct Col3Lg {
   static constexpr int E = 8;
-  static constexpr int T = L / E;           // threads of one line
-  static constexpr int W = col3_tile_w(L);  // columns per tile
+  static constexpr int T = L / E;  // threads of one line
+  static constexpr int W = WT;     // columns per tile
   static constexpr int LGW = ilog2(W);
-  static constexpr int NC = 3;
+  static constexpr int NC = NCT;
   static constexpr int NL = NC * W;  // lines per tile
   static constexpr int THREADS = NL * T;
   static constexpr int LP = Plan<L, E>::LP;
   static constexpr int XS = LP;         // a line's own exchange buffer inside the slot
   static constexpr int SLOT = NL * XS;  // >= NL * L landing
-  static constexpr int NSLOT = 2;
+  static constexpr int NSLOT = NS;
   // (+ 1024: the kernel aligns its slots inside the dynamic segment)
   static constexpr int SMEM = (NSLOT * SLOT + L / 2) * (int)sizeof(double2) + 1024;
   static constexpr unsigned TX = (unsigned)(NL * L * sizeof(double2));
@@ -75,10 +77,26 @@ struct Col3Lg {
   static_assert((SLOT * 16) % 1024 == 0, "slots keep the 1024-byte swizzle alignment");
   static_assert(NL <= 15 || T == 32, "one named barrier per line");
   static_assert(SMEM + 2048 <= 232448, "shared memory budget (with the kernel's static variables)");
+  static_assert(NC == 3 || NC == 1, "whole vectors or single components");
   // entry of (component c, line position pos, column w) in the swizzled landing layout
   __device__ static __forceinline__ int land(int c, int pos, int w) {
     return ((c * L + pos) << LGW) | (w ^ ((pos >> (3 - LGW)) & (W - 1)));
   }
+};
+
+// Plain y passes on single-component tiles: 8 columns (128-byte box rows: half
+// the TMA requests per byte of the 4-column vector tiles) and three slots, so
+// the load of tile k+2, the transform of tile k and the store of tile k-1
+// overlap.  Measured SLOWER where it ran (256^3: y forward 282 -> 314 us, y
+// inverse 240 -> 270 us per field) and the 512-line form did not come up on the
+// z-blocked maps, so the vector tiles stay (FFTC_COL3_Y1 = 1 builds it).
+#ifndef FFTC_COL3_Y1
+#define FFTC_COL3_Y1 0
+#endif
+template <int L>
+struct Col3YSel {
+  static constexpr bool Y1 = FFTC_COL3_Y1 && L <= 512;
+  using type = Col3Lg<L, Y1 ? 1 : 3, Y1 ? 8 : col3_tile_w(L), Y1 ? 3 : 2>;
 };
 
 // barrier over the T threads of one line
@@ -98,37 +116,41 @@ struct LineSync {
 // PEER: outputs go straight to their owning rank (PeerOut po) as bulk copies
 // of whole tile rows -- the decomposed solve's transposes fused into the pass
 // that produces the data (staged unswizzled: a bulk copy reads raw bytes).
-template <int MODE, int L, bool PEER = false>
-__global__ void __launch_bounds__(Col3Lg<L>::THREADS, 1)
+template <int MODE, int L, bool PEER = false, class K = Col3Lg<L>>
+__global__ void __launch_bounds__(K::THREADS, 1)
     k_col3_lg(Args a, Line3 g, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const PeerOut* __restrict__ po) {
-  using K = Col3Lg<L>;
-  constexpr int E = K::E, T = K::T, W = K::W;
+  constexpr int E = K::E, T = K::T, W = K::W, NC = K::NC;
   constexpr bool MID = (MODE == MID_BASIC || MODE == MID_EM);
   constexpr bool INV_ONLY = (MODE == COL_INV);
+  static_assert(!MID || NC == 3, "the projection needs whole vectors");
   extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ uint64_t bars[K::NSLOT];
   if (!a.op_mode && a.st->stopped) return;
   // slots on 1024-byte boundaries of the shared window: the swizzle is a function of the slot offset
   double2* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / (unsigned)sizeof(double2);
-  const int t = threadIdx.x % T, line = threadIdx.x / T, w = line % W, comp = line / W;
+  // (NC = 1: the tile's component comes with the tile, lcomp = 0 in the slot)
+  const int t = threadIdx.x % T, line = threadIdx.x / T, w = line % W, lcomp = line / W;
   const int nstrips = a.nx / W;
   // Tiles of one field go round robin over the CTAs, field after field, so a
   // pass over field B alone (Line3::f0 = 1, the memory-lean schedule) deals a
   // CTA the same flux tiles in the same order as the two-field pass does.
-  const int per_field = g.nouter * nstrips;
+  const int per_comp = g.nouter * nstrips;
+  const int per_field = per_comp * (3 / NC);
   const int nper = (int)blockIdx.x < per_field ? (per_field - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   const int nmine = nper * g.nfields;
-  auto coords = [&](int k, int& f, int& o, int& x0) {
+  auto coords = [&](int k, int& f, int& o, int& x0, int& c0) {
     // (nfields <= 2)
 #if FFTC_COL3_ALT
     const int fl = g.nfields == 2 ? (k & 1) : 0;
-    const int r = (int)blockIdx.x + (g.nfields == 2 ? (k >> 1) : k) * (int)gridDim.x;
+    int r = (int)blockIdx.x + (g.nfields == 2 ? (k >> 1) : k) * (int)gridDim.x;
 #else
     const int fl = k >= nper ? 1 : 0;
-    const int r = (int)blockIdx.x + (k - fl * nper) * (int)gridDim.x;
+    int r = (int)blockIdx.x + (k - fl * nper) * (int)gridDim.x;
 #endif
     f = g.f0 + fl;
+    c0 = NC == 1 ? r / per_comp : 0;  // single-component tiles: component slowest
+    r -= c0 * per_comp;
     o = r / nstrips;
     x0 = (r - o * nstrips) * W;
   };
@@ -139,15 +161,9 @@ __global__ void __launch_bounds__(Col3Lg<L>::THREADS, 1)
   __syncthreads();
   if (threadIdx.x == 0)
     for (int j = 0; j < K::NSLOT - 1 && j < nmine; ++j) {
-      int f, o, x0;
-      coords(j, f, o, x0);
-      col3_issue(f == 0 ? &tmA : &tmB, smem + j * K::SLOT, &bars[j], x0, col3_outer(g, o), K::TX);
-#if FFTC_COL3_PF
-      if (j + 1 < nmine) {
-        coords(j + 1, f, o, x0);
-        col3_prefetch(f == 0 ? &tmA : &tmB, x0, col3_outer(g, o));
-      }
-#endif
+      int f, o, x0, c0;
+      coords(j, f, o, x0, c0);
+      col3_issue(f == 0 ? &tmA : &tmB, smem + j * K::SLOT, &bars[j], x0, col3_outer(g, o), K::TX, c0);
     }
   double2* tws = smem + K::NSLOT * K::SLOT;
   for (int i = threadIdx.x; i < L / 2; i += blockDim.x) tws[tw_swz(i)] = __ldg(&a.tw[g.axis][i]);
@@ -157,31 +173,32 @@ __global__ void __launch_bounds__(Col3Lg<L>::THREADS, 1)
   double acc = 0.0;
   for (int k = 0; k < nmine; ++k) {
     const int s = k % K::NSLOT;
-    int f, o, x0;
-    coords(k, f, o, x0);
+    int f, o, x0, c0;
+    coords(k, f, o, x0, c0);
+    const int comp = NC == 1 ? c0 : lcomp;
     double2* slot = smem + s * K::SLOT;
     mbar_wait(&bars[s], (unsigned)((k / K::NSLOT) & 1));
     double2 v[1][E];
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[0][i] = slot[K::land(comp, pos_first<L, E>(INV_ONLY, t, i), w)];
-    // (peer bulk copies: each thread's copies out of the other slot have been
-    // read before thread 0 reloads it below)
+    for (int i = 0; i < E; ++i) v[0][i] = slot[K::land(lcomp, pos_first<L, E>(INV_ONLY, t, i), w)];
+    // (peer bulk copies: each thread's copies out of the slot reloaded below
+    // have been read before thread 0 reloads it)
     if constexpr (PEER) bulk_wait_read0();
     __syncthreads();  // every input is in registers: the slot becomes the lines' exchange scratch
     if (threadIdx.x == 0 && k + K::NSLOT - 1 < nmine) {
       // tile k+NSLOT-1 into the slot of tile k-1, whose store was committed one tile ago
       const int nk = k + K::NSLOT - 1;
-      int nf, no, nx0;
-      coords(nk, nf, no, nx0);
+      int nf, no, nx0, nc0;
+      coords(nk, nf, no, nx0, nc0);
 #if FFTC_COL3_PF
       if (nk + 1 < nmine) {  // the tile after it: DRAM -> L2 while this one is transformed
-        int pf, po_, px0;
-        coords(nk + 1, pf, po_, px0);
+        int pf, po_, px0, pc0;
+        coords(nk + 1, pf, po_, px0, pc0);
         col3_prefetch(pf == 0 ? &tmA : &tmB, px0, col3_outer(g, po_));
       }
 #endif
       col3_issue(nf == 0 ? &tmA : &tmB, smem + (nk % K::NSLOT) * K::SLOT, &bars[nk % K::NSLOT], nx0, col3_outer(g, no),
-                 K::TX);
+                 K::TX, nc0);
     }
     double2* xb = slot + line * K::XS;  // this line's own buffer
     const bool parseval_only = (MODE == MID_EM) && f == 1;
@@ -261,12 +278,13 @@ __global__ void __launch_bounds__(Col3Lg<L>::THREADS, 1)
         // line position): the tile's W adjacent x-values are one contiguous
         // 16W-byte run in the owning rank's slab (NVLink to peers).
 #pragma unroll
-        for (int i = 0; i < E; ++i) slot[(comp * L + pos_last<L, E>(inv_layout, t, i)) * W + w] = v[0][i];
+        for (int i = 0; i < E; ++i) slot[(lcomp * L + pos_last<L, E>(inv_layout, t, i)) * W + w] = v[0][i];
         fence_proxy_async();
         __syncthreads();
         const int rq = po->rows_per_rank;
-        for (int r = threadIdx.x; r < 3 * L; r += (int)blockDim.x) {
-          const int cc = r / L, pos = r - cc * L;
+        for (int r = threadIdx.x; r < NC * L; r += (int)blockDim.x) {
+          const int lc = r / L, pos = r - lc * L;
+          const int cc = NC == 1 ? comp : lc;
           const int q = pos / rq;
           const long long p = pos - q * rq;
           long long off;
@@ -279,16 +297,16 @@ __global__ void __launch_bounds__(Col3Lg<L>::THREADS, 1)
           } else {
             off = cc * po->comp_stride + (po->outer0 + o) * po->outer_stride + x0 + p * po->line_stride;
           }
-          bulk_s2g(po->dst[f][q] + off, slot + (cc * L + pos) * W, (unsigned)(W * sizeof(double2)));
+          bulk_s2g(po->dst[f][q] + off, slot + (lc * L + pos) * W, (unsigned)(W * sizeof(double2)));
         }
         bulk_commit();
       } else {
 #pragma unroll
-        for (int i = 0; i < E; ++i) slot[K::land(comp, pos_last<L, E>(inv_layout, t, i), w)] = v[0][i];
+        for (int i = 0; i < E; ++i) slot[K::land(lcomp, pos_last<L, E>(inv_layout, t, i), w)] = v[0][i];
         fence_proxy_async();
         __syncthreads();
         if (threadIdx.x == 0) {
-          col3_store(f == 0 ? &tmA : &tmB, slot, x0, col3_outer(g, o));
+          col3_store(f == 0 ? &tmA : &tmB, slot, x0, col3_outer(g, o), c0);
           bulk_commit();
         }
       }

@@ -57,18 +57,18 @@ __device__ __forceinline__ int2 col3_outer(const Line3& g, int o) {
   return g.om > 0 ? make_int2((o >> g.obs) * g.om, o & ((1 << g.obs) - 1)) : make_int2(0, o);
 }
 __device__ __forceinline__ void col3_issue(const CUtensorMap* tm, double2* slot, uint64_t* bar, int x0, int2 oc,
-                                           unsigned tx) {
+                                           unsigned tx, int c0 = 0) {
   bulk_wait_read0();  // the TMA store that last used this slot has read it out
   mbar_expect_tx(bar, tx);
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
       "%6}], [%7];" ::"r"(smem_u32(slot)),
-      "l"(tm), "r"(2 * x0), "r"(0), "r"(oc.x), "r"(oc.y), "r"(0), "r"(smem_u32(bar))
+      "l"(tm), "r"(2 * x0), "r"(0), "r"(oc.x), "r"(oc.y), "r"(c0), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2* slot, int x0, int2 oc) {
+__device__ __forceinline__ void col3_store(const CUtensorMap* tm, const double2* slot, int x0, int2 oc, int c0 = 0) {
   asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(tm),
-               "r"(2 * x0), "r"(0), "r"(oc.x), "r"(oc.y), "r"(0), "r"(smem_u32(slot))
+               "r"(2 * x0), "r"(0), "r"(oc.x), "r"(oc.y), "r"(c0), "r"(smem_u32(slot))
                : "memory");
 }
 

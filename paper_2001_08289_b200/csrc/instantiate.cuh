@@ -90,6 +90,19 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID3P_EM] = FFTC_K3(MID_EM, true);
     t.col[KC_FWD3P] = FFTC_K3(COL_FWD, true);
 #undef FFTC_K3
+#if FFTC_COL3_LG
+    {  // plain y passes: single-component tiles where the line length allows (Col3YSel)
+      using KY = typename Col3YSel<LL>::type;
+      t.col[KC_FWD3T] = make(k_col3_lg<COL_FWD, LL, false, KY>, KY::THREADS, KY::SMEM, 1);
+      t.col[KC_INV3T] = make(k_col3_lg<COL_INV, LL, false, KY>, KY::THREADS, KY::SMEM, 1);
+      t.col[KC_FWD3P] = make(k_col3_lg<COL_FWD, LL, true, KY>, KY::THREADS, KY::SMEM, 1);
+      for (int kc : {KC_FWD3T, KC_INV3T, KC_FWD3P}) {
+        t.col[kc].swz = KY::W;
+        t.col[kc].tile_w = KY::W;
+        t.col[kc].tile_nc = KY::NC;
+      }
+    }
+#endif
 #if FFTC_COL3_LG && FFTC_COL3_MID3
     using KM = Col3Mid<LL>;
     t.col[KC_MID3T_BASIC] = make(k_col3_mid<MID_BASIC, LL, false>, KM::THREADS, KM::SMEM, 1);

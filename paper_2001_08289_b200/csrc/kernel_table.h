@@ -12,6 +12,8 @@ struct KInfo {
   int lines = 0;       // lines processed per CTA per loop trip (G)
   int max_active = 0;  // resident CTAs per SM (filled at first use)
   int swz = 0;         // 3-D TMA column passes: tensor maps swizzled over one box row (cols3_lg.cuh)
+  int tile_w = 0;      // 3-D TMA column passes: columns per tile (0: col3_tile_w(L))
+  int tile_nc = 0;     // ... components per tile (0: 3)
 };
 
 // column kernel variants
