@@ -103,6 +103,17 @@ inline void fill_tma(LTable& t) {
       }
     }
 #endif
+#if FFTC_COL3_LG
+    // lines of 1024 (two-column tiles, four warps per line): the plain y passes
+    // measured 4-8 % faster on the round-1 mapping (1024^3: y forward 24.7 vs
+    // 25.7 ms, y inverse 21.1 vs 23.0 ms), so they keep it, on unswizzled maps
+    if constexpr (LL == 1024) {
+      using KO = Col3Tma<LL>;
+      t.col[KC_FWD3T] = make(k_col3_tma<COL_FWD, LL, false>, KO::THREADS, KO::SMEM, 1);
+      t.col[KC_INV3T] = make(k_col3_tma<COL_INV, LL, false>, KO::THREADS, KO::SMEM, 1);
+      t.col[KC_FWD3P] = make(k_col3_tma<COL_FWD, LL, true>, KO::THREADS, KO::SMEM, 1);
+    }
+#endif
 #if FFTC_COL3_LG && FFTC_COL3_MID3
     using KM = Col3Mid<LL>;
     t.col[KC_MID3T_BASIC] = make(k_col3_mid<MID_BASIC, LL, false>, KM::THREADS, KM::SMEM, 1);
