@@ -1,7 +1,7 @@
 // cols3_lg.cuh -- TMA-staged column passes of 3-D fields, line-group form
 // (the y passes and the z pass with the Gamma projection, lines of 256..1024).
 //
-// Same algebra and the same tiles as cols3_tma.cuh (spectral_ops.py:120-128
+// Same algebra and the same tiles as round 1's k_col3_tma (spectral_ops.py:120-128
 // in 3-D: a tile is W adjacent x-columns of all three components along the
 // line axis, one cp.async.bulk.tensor per tile, two slots).  What changes is
 // who synchronises with whom.  There a line's T threads were spread over all
@@ -88,8 +88,8 @@ struct Col3Lg {
 // the TMA requests per byte of the 4-column vector tiles) and three slots, so
 // the load of tile k+2, the transform of tile k and the store of tile k-1
 // overlap.  Measured SLOWER where it ran (256^3: y forward 282 -> 314 us, y
-// inverse 240 -> 270 us per field) and the 512-line form did not come up on the
-// z-blocked maps, so the vector tiles stay (FFTC_COL3_Y1 = 1 builds it).
+// inverse 240 -> 270 us per field), so the vector tiles stay (FFTC_COL3_Y1 = 1
+// builds it).
 #ifndef FFTC_COL3_Y1
 #define FFTC_COL3_Y1 0
 #endif

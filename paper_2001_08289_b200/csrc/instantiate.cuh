@@ -74,13 +74,8 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID2T_EM] = make(k_mid2_tma<MID_EM, LL>, ColTma<LL>::THREADS, ColTma<LL>::SMEM, 1);
   }
   if constexpr (LL >= 256 && LL <= 1024) {  // TMA tensor-map 3-D column passes
-#if FFTC_COL3_LG
     using K3 = Col3Lg<LL>;
 #define FFTC_K3(MODE, PEER) make(k_col3_lg<MODE, LL, PEER>, K3::THREADS, K3::SMEM, 1)
-#else
-    using K3 = Col3Tma<LL>;
-#define FFTC_K3(MODE, PEER) make(k_col3_tma<MODE, LL, PEER>, K3::THREADS, K3::SMEM, 1)
-#endif
     static_assert(K3::W == col3_tile_w(LL), "host and device tile widths agree");
     t.col[KC_MID3T_BASIC] = FFTC_K3(MID_BASIC, false);
     t.col[KC_MID3T_EM] = FFTC_K3(MID_EM, false);
@@ -90,8 +85,9 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID3P_EM] = FFTC_K3(MID_EM, true);
     t.col[KC_FWD3P] = FFTC_K3(COL_FWD, true);
 #undef FFTC_K3
-#if FFTC_COL3_LG
-    {  // plain y passes: single-component tiles where the line length allows (Col3YSel)
+    for (int kc : {KC_MID3T_BASIC, KC_MID3T_EM, KC_FWD3T, KC_INV3T, KC_MID3P_BASIC, KC_MID3P_EM, KC_FWD3P})
+      t.col[kc].swz = K3::W;
+    if constexpr (Col3YSel<LL>::Y1) {  // plain y passes on single-component tiles (off by default)
       using KY = typename Col3YSel<LL>::type;
       t.col[KC_FWD3T] = make(k_col3_lg<COL_FWD, LL, false, KY>, KY::THREADS, KY::SMEM, 1);
       t.col[KC_INV3T] = make(k_col3_lg<COL_INV, LL, false, KY>, KY::THREADS, KY::SMEM, 1);
@@ -102,27 +98,14 @@ inline void fill_tma(LTable& t) {
         t.col[kc].tile_nc = KY::NC;
       }
     }
-#endif
-#if FFTC_COL3_LG
-    // lines of 1024 (two-column tiles, four warps per line): the plain y passes
-    // measured 4-8 % faster on the round-1 mapping (1024^3: y forward 24.7 vs
-    // 25.7 ms, y inverse 21.1 vs 23.0 ms), so they keep it, on unswizzled maps
-    if constexpr (LL == 1024) {
-      using KO = Col3Tma<LL>;
-      t.col[KC_FWD3T] = make(k_col3_tma<COL_FWD, LL, false>, KO::THREADS, KO::SMEM, 1);
-      t.col[KC_INV3T] = make(k_col3_tma<COL_INV, LL, false>, KO::THREADS, KO::SMEM, 1);
-      t.col[KC_FWD3P] = make(k_col3_tma<COL_FWD, LL, true>, KO::THREADS, KO::SMEM, 1);
-    }
-#endif
-#if FFTC_COL3_LG && FFTC_COL3_MID3
+#if FFTC_COL3_MID3
     using KM = Col3Mid<LL>;
     t.col[KC_MID3T_BASIC] = make(k_col3_mid<MID_BASIC, LL, false>, KM::THREADS, KM::SMEM, 1);
     t.col[KC_MID3T_EM] = make(k_col3_mid<MID_EM, LL, false>, KM::THREADS, KM::SMEM, 1);
     t.col[KC_MID3P_BASIC] = make(k_col3_mid<MID_BASIC, LL, true>, KM::THREADS, KM::SMEM, 1);
     t.col[KC_MID3P_EM] = make(k_col3_mid<MID_EM, LL, true>, KM::THREADS, KM::SMEM, 1);
+    for (int kc : {KC_MID3T_BASIC, KC_MID3T_EM, KC_MID3P_BASIC, KC_MID3P_EM}) t.col[kc].swz = KM::W;
 #endif
-    for (int kc : {KC_MID3T_BASIC, KC_MID3T_EM, KC_FWD3T, KC_INV3T, KC_MID3P_BASIC, KC_MID3P_EM, KC_FWD3P})
-      t.col[kc].swz = FFTC_COL3_LG ? K3::W : 0;
   }
   if constexpr (LL >= FFTC_TMA_ROWS_MIN) {  // TMA-staged persistent row sweeps
 #define FFTC_TMA(SCH)                                                                                   \

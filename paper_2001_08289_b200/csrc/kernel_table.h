@@ -22,13 +22,9 @@ enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_
        KC_MID3T_BASIC = 8, KC_MID3T_EM = 9, KC_FWD3T = 10, KC_INV3T = 11,  // 3-D (Args, Line3, map A, map B, PeerOut*)
        KC_MID3P_BASIC = 12, KC_MID3P_EM = 13, KC_FWD3P = 14,  // the same, outputs to their owning ranks
        KC_COUNT = 15 };
-// columns per TMA tile of the 3-D column passes (cols3_tma.cuh: Col3Tma<L>::W)
+// columns per TMA tile of the 3-D column passes (cols3_lg.cuh: Col3Lg<L>::W)
 #ifndef FFTC_COL3_W512
 #define FFTC_COL3_W512 4
-#endif
-// line-group form of the 3-D TMA column passes (cols3_lg.cuh); 0: cols3_tma.cuh
-#ifndef FFTC_COL3_LG
-#define FFTC_COL3_LG 1
 #endif
 // z pass with three components per thread (k_col3_mid); 0: one component per thread
 #ifndef FFTC_COL3_MID3

@@ -105,6 +105,16 @@ def test_3d_configs_first_iterations_at_size(g):
         _same_to_roundoff(r, rl)
 
 
+@pytest.mark.parametrize("g", _cases("c3full"))
+def test_c3_full_solve_at_size(g):
+    """BASELINE configs[2] itself: the whole 512^3 em_sub solve against the
+    bounded-memory oracle's record (every iteration's sigma* and residual,
+    the iteration count and status; the fixture keeps no fields).  Present
+    when oracle/gen_golden.py c3full has been run (hours of CPU)."""
+    r = run_case(g["case"])
+    check(r, g)
+
+
 def _lean_pair(chi, sigma1, e0, max_iters, fields):
     import paper_2001_08289_b200 as fb
     from paper_2001_08289_b200 import native
