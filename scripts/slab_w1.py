@@ -48,3 +48,10 @@ for name, fn in ((k, v) for k, v in variants.items() if k in only):
     it = r.iterations if hasattr(r, "iterations") else r["iterations"]
     fused = r.get("fused") if isinstance(r, dict) else None
     print(f"{n}^3 {scheme} {name:14s} {1e3 * dt / it:8.2f} ms/iter ({it} iters, fused={fused})", flush=True)
+    if os.environ.get("SLAB_STATS"):  # per-kernel device time of one more run (profile mode: events around every launch)
+        from paper_2001_08289_b200 import native
+        native.profile(True)
+        fn()
+        st = native.kernel_stats()
+        native.profile(False)
+        print("   ", " ".join(f"{k} {1e3 * v[1] / max(v[0], 1):.0f}us x{v[0]}" for k, v in st.items()), flush=True)
