@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(Col3Mid<L>::THREADS, 1)
   using K = Col3Mid<L>;
   using KG = Col3Lg<L>;
   constexpr int E = K::E, T = K::T, W = K::W, NC = K::NC;
-  static_assert(MODE == MID_BASIC || MODE == MID_EM, "the projection pass");
+  constexpr bool MID = (MODE == MID_BASIC || MODE == MID_EM);  // else a plain y pass, three components per thread
+  constexpr bool INV_ONLY = (MODE == COL_INV);
   extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ uint64_t bars[K::NSLOT];
   if (!a.op_mode && a.st->stopped) return;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(Col3Mid<L>::THREADS, 1)
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int i = 0; i < E; ++i) v[c][i] = slot[KG::land(c, pos_first<L, E>(false, t, i), w)];
+      for (int i = 0; i < E; ++i) v[c][i] = slot[KG::land(c, pos_first<L, E>(INV_ONLY, t, i), w)];
     if constexpr (PEER) bulk_wait_read0();
     __syncthreads();  // every input is in registers: the slot becomes the columns' exchange scratch
     if (threadIdx.x == 0 && k + K::NSLOT - 1 < nmine) {
@@ -416,7 +417,8 @@ __global__ void __launch_bounds__(Col3Mid<L>::THREADS, 1)
     const bool parseval_only = (MODE == MID_EM) && f == 1;
     // (no tail barrier: the projection touches no shared memory, and the
     // inverse's first exchange is preceded by the column barrier below)
-    fft_line<L, E, NC, false, false>(v, t, tw, xb, lsync);
+    if constexpr (!INV_ONLY) fft_line<L, E, NC, false, false>(v, t, tw, xb, lsync);
+    if constexpr (MID) {
     // Gamma projection (spectral_ops.py:124-127), k = (kx, k_outer, k_line)
     const double kx = (double)wavenum(x0 + w, a.nx), ko = (double)wavenum(g.o0 + o, g.on);
     const double kxo2 = kx * kx + ko * ko;
@@ -449,15 +451,17 @@ __global__ void __launch_bounds__(Col3Mid<L>::THREADS, 1)
         }
       }
     }
+    }  // MID
     if (!parseval_only) {
-      lsync();  // the column's last forward exchange reads are done
-      fft_line<L, E, NC, true, false>(v, t, tw, xb, lsync);
+      if constexpr (MID) lsync();  // the column's last forward exchange reads are done
+      if constexpr (MODE != COL_FWD) fft_line<L, E, NC, true, false>(v, t, tw, xb, lsync);
+      constexpr bool inv_layout = (MODE != COL_FWD);
       __syncthreads();  // every column's exchange reads are done before outputs overwrite the slot
       if constexpr (PEER) {
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
-          for (int i = 0; i < E; ++i) slot[(c * L + pos_last<L, E>(true, t, i)) * W + w] = v[c][i];
+          for (int i = 0; i < E; ++i) slot[(c * L + pos_last<L, E>(inv_layout, t, i)) * W + w] = v[c][i];
         fence_proxy_async();
         __syncthreads();
         const int rq = po->rows_per_rank;
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(Col3Mid<L>::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
-          for (int i = 0; i < E; ++i) slot[KG::land(c, pos_last<L, E>(true, t, i), w)] = v[c][i];
+          for (int i = 0; i < E; ++i) slot[KG::land(c, pos_last<L, E>(inv_layout, t, i), w)] = v[c][i];
         fence_proxy_async();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -497,10 +501,12 @@ __global__ void __launch_bounds__(Col3Mid<L>::THREADS, 1)
   }
   if (threadIdx.x == 0 || PEER) bulk_wait0();  // stores have landed in global memory
   if constexpr (PEER) __threadfence_system();  // peer stores visible before the host-level barrier
-  double in[1] = {acc}, tot[1];
-  if (grid_reduce<1>(in, tot, a) && threadIdx.x == 0 && !a.op_mode && !g.no_monitor) {
-    if (a.dist) a.st->parseval = tot[0] / a.inv_n;
-    else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
+  if constexpr (MID) {
+    double in[1] = {acc}, tot[1];
+    if (grid_reduce<1>(in, tot, a) && threadIdx.x == 0 && !a.op_mode && !g.no_monitor) {
+      if (a.dist) a.st->parseval = tot[0] / a.inv_n;
+      else monitor_step(a, tot[0] / a.inv_n + a.st->js2);
+    }
   }
 }
 

@@ -105,6 +105,12 @@ inline void fill_tma(LTable& t) {
     t.col[KC_MID3P_BASIC] = make(k_col3_mid<MID_BASIC, LL, true>, KM::THREADS, KM::SMEM, 1);
     t.col[KC_MID3P_EM] = make(k_col3_mid<MID_EM, LL, true>, KM::THREADS, KM::SMEM, 1);
     for (int kc : {KC_MID3T_BASIC, KC_MID3T_EM, KC_MID3P_BASIC, KC_MID3P_EM}) t.col[kc].swz = KM::W;
+#if FFTC_COL3_Y3C  // plain y passes on the same three-components-per-thread form
+    t.col[KC_FWD3T] = make(k_col3_mid<COL_FWD, LL, false>, KM::THREADS, KM::SMEM, 1);
+    t.col[KC_INV3T] = make(k_col3_mid<COL_INV, LL, false>, KM::THREADS, KM::SMEM, 1);
+    t.col[KC_FWD3P] = make(k_col3_mid<COL_FWD, LL, true>, KM::THREADS, KM::SMEM, 1);
+    for (int kc : {KC_FWD3T, KC_INV3T, KC_FWD3P}) t.col[kc].swz = KM::W;
+#endif
 #endif
   }
   if constexpr (LL >= FFTC_TMA_ROWS_MIN) {  // TMA-staged persistent row sweeps

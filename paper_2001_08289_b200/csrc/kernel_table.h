@@ -30,6 +30,10 @@ enum { KC_MID2_BASIC = 0, KC_MID2_EM = 1, KC_MID3_BASIC = 2, KC_MID3_EM = 3, KC_
 #ifndef FFTC_COL3_MID3
 #define FFTC_COL3_MID3 1
 #endif
+// plain y passes with three components per thread too (k_col3_mid<COL_FWD/COL_INV>)
+#ifndef FFTC_COL3_Y3C
+#define FFTC_COL3_Y3C 0
+#endif
 constexpr int col3_tile_w(long long L) { return L <= 256 ? 8 : (L <= 512 ? FFTC_COL3_W512 : 2); }
 
 struct LTable {
