@@ -201,7 +201,7 @@ bool make_field_map(CUtensorMap* tm, void* base, long long nx, long long ny, int
 // 5-D map for the 3-D column passes: lines of length L at element stride
 // line_stride, nouter of them at outer_stride, three components at
 // comp_stride; a box is W adjacent x-columns of all three components
-// {2W doubles, 256 rows, L/256 blocks, 1, 3} (cols3_tma.cuh).
+// {2W doubles, 256 rows, L/256 blocks, 1, 3} (cols3_lg.cuh).
 // swz > 0: the TMA swizzle whose span is one box row (16 W bytes), cols3_lg.cuh
 CUtensorMapSwizzle col3_swizzle(int swz) {
   return swz == 8 ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -813,7 +813,7 @@ int fftc_solve(const fftc_problem* pb, const fftc_params* pr, double* history, i
       yf.ostride = nx * ny;
       yf.nstrips = (int)(nx / 2);
     }
-    // 3-D TMA column passes (cols3_tma.cuh) where the line lengths allow
+    // 3-D TMA column passes (cols3_lg.cuh) where the line lengths allow
     Col3Pass zmid, yfwd, yinv, zpar;
     const PeerOut* no_peer = nullptr;
     a.zbs = 0;

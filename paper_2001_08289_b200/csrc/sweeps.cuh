@@ -653,7 +653,7 @@ struct ColGeom {
   int pad;
 };
 
-// geometry of a TMA 3-D column pass (cols3_tma.cuh)
+// geometry of a TMA 3-D column pass (cols3_lg.cuh)
 struct Line3 {
   int nouter;   // outer lines per field (z for the y passes, y for the z pass)
   int o0, on;   // global index of outer 0 and the outer axis extent (wave numbers)

@@ -158,7 +158,7 @@ def test_repeat_determinism_long_em_sub():
                                            ((512, 256, 4), "em"), ((1024, 256, 2), "basic_sub")])
 def test_3d_tma_column_passes_vs_oracle(shape, scheme):
     """Grids whose y and z lines (256..1024) run the TMA tile kernels
-    (cols3_tma.cuh), against the oracle restatement (pinned to the reference
+    (cols3_lg.cuh), against the oracle restatement (pinned to the reference
     by the 2-D goldens and the 2-D embedding check)."""
     import paper_2001_08289_b200 as fb
     from oracle import fftcond_oracle as O
