@@ -27,7 +27,7 @@ namespace fftc {
 #define FFTC_ROW512_MINB1 4
 #endif
 #ifndef FFTC_ROW512_MINB3
-#define FFTC_ROW512_MINB3 8
+#define FFTC_ROW512_MINB3 6
 #endif
 // em_sub sweep 1 on 8-per-thread rows: both channels (Rq, Jq) in one thread
 // (1), or split over two thread groups with a shared-memory handoff (0)
