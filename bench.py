@@ -921,8 +921,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=WORKLOADS, default="c3")
     ap.add_argument("--e2e-steps", type=int, default=3, help="end-to-end steps (at most --steps)")
-    ap.add_argument("--ref-iters", type=int, default=20,
-                    help="2-D reference arm: iterations per sample (BASELINE.md section 2: k = 20)")
+    ap.add_argument("--ref-iters", type=int, default=8,
+                    help="2-D reference arm: iterations per concurrent sample (one sample per host core; k = 20 of "
+                         "BASELINE.md section 2 takes ~90 s per step at 2048^2 on 16 cores, the one-core cpu_baseline "
+                         "leg uses k = 20)")
     ap.add_argument("--cpu-iters", type=int, default=20, help="2-D cpu_baseline: iterations per solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c5-points", type=int, default=256)
