@@ -93,10 +93,18 @@ struct Col3Lg {
 #ifndef FFTC_COL3_Y1
 #define FFTC_COL3_Y1 0
 #endif
+// Lines of 1024: the vector tiles are two columns wide (32-byte box rows), and
+// ncu shows the passes re-reading DRAM (1024^3: 70.1 GB read per launch
+// against 51.5 GB algorithmic -- half-used 64-byte DRAM atoms whose other half
+// is gone from L2 when the neighbouring tile asks for it).  Single-component
+// tiles there are four columns wide (64-byte rows, three slots).
+#ifndef FFTC_COL3_Y1_1024
+#define FFTC_COL3_Y1_1024 1
+#endif
 template <int L>
 struct Col3YSel {
-  static constexpr bool Y1 = FFTC_COL3_Y1 && L <= 512;
-  using type = Col3Lg<L, Y1 ? 1 : 3, Y1 ? 8 : col3_tile_w(L), Y1 ? 3 : 2>;
+  static constexpr bool Y1 = (FFTC_COL3_Y1 && L <= 512) || (FFTC_COL3_Y1_1024 && L == 1024);
+  using type = Col3Lg<L, Y1 ? 1 : 3, Y1 ? (L == 1024 ? 4 : 8) : col3_tile_w(L), Y1 ? 3 : 2>;
 };
 
 // barrier over the T threads of one line
