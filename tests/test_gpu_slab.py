@@ -144,7 +144,8 @@ def _run_threads(chi, cfg, world, fused=True):
 
 @pytest.mark.parametrize("fused", [False, True], ids=["alltoall", "fused"])
 @pytest.mark.parametrize("shape, scheme, world", [((256, 256, 8), "em_sub", 2), ((256, 256, 8), "basic", 4),
-                                                  ((512, 256, 8), "em", 2), ((64, 64, 64), "basic_sub", 4)])
+                                                  ((512, 256, 8), "em", 2), ((64, 64, 64), "basic_sub", 4),
+                                                  ((256, 1024, 8), "em", 2)])
 def test_slab_threads_match_monolithic(shape, scheme, world, fused):
     """z-slab decomposition at world 2 / 4 on the GPU kernels (rank-local
     slabs with y0/z0 offsets, TMA tile column passes where the line lengths
@@ -161,10 +162,11 @@ def test_slab_threads_match_monolithic(shape, scheme, world, fused):
     recs = _run_threads(chi, cfg, world, fused)
     # fused transposes need the TMA tile passes: y and z lines of 256..1024 and
     # nx a multiple of their tile widths; the 64^3 case keeps the all-to-alls
-    def tile_ok(n):
-        return 256 <= n <= 1024 and shape[2] % (8 if n <= 256 else 4 if n <= 512 else 2) == 0
+    # (y lines of 1024 run single-component tiles of four columns, z lines of 1024 vector tiles of two)
+    def tile_ok(n, y_lines):
+        return 256 <= n <= 1024 and shape[2] % (8 if n <= 256 else 4 if n <= 512 else (4 if y_lines else 2)) == 0
 
-    assert all(r["fused"] == (fused and tile_ok(shape[0]) and tile_ok(shape[1])) for r in recs)
+    assert all(r["fused"] == (fused and tile_ok(shape[0], False) and tile_ok(shape[1], True)) for r in recs)
     for r in recs:
         assert r["world"] == world and r["iterations"] == mono.iterations
         assert r["status"] == mono.status
